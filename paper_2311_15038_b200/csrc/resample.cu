@@ -1,0 +1,140 @@
+// General-ratio box downscale and slicemap atlas packing (device side).
+//
+//   ctp_downscale_u8     <- volume.py:277-309 downscale_volume (+ _cell_starts, volume.py:265-274)
+//   ctp_encode_atlas_u8  <- slicemap.py:120-142 packing + pipeline.py:226-237 _pad_to_cube
+//   ctp_decode_atlas_u8  <- slicemap.py:145-155 decode_slicemaps
+//
+// The fused power-of-two pyramid lives in preview.cu; this file covers the
+// non-integer ratios (e.g. the 160 -> 128 level of demo-scan-01 or 768 -> 512
+// of config 5), which assign each source voxel to the cell containing its
+// centre, so cells hold floor(n/t) or ceil(n/t) voxels per axis.
+#include "ctp_common.cuh"
+
+namespace ctp {
+
+// start[j] = ceil((2 j n - t) / (2 t)), start[0] = 0, start[t] = n (volume.py:265-274)
+__device__ __forceinline__ int64_t cell_start(int64_t j, int64_t n, int64_t t) {
+  if (j <= 0) return 0;
+  if (j >= t) return n;
+  const int64_t num = 2 * j * n - t;  // > 0 for j >= 1 since t <= n
+  return (num + 2 * t - 1) / (2 * t);
+}
+
+__global__ void downscale_u8_kernel(const uint8_t* __restrict__ in, int64_t nz, int64_t ny, int64_t nx,
+                                    int64_t tz, int64_t ty, int64_t tx, uint8_t* __restrict__ out) {
+  const int64_t total = tz * ty * tx;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jx = o % tx;
+    const int64_t r = o / tx;
+    const int64_t jy = r % ty;
+    const int64_t jz = r / ty;
+    const int64_t xa = cell_start(jx, nx, tx), xb = cell_start(jx + 1, nx, tx);
+    const int64_t ya = cell_start(jy, ny, ty), yb = cell_start(jy + 1, ny, ty);
+    const int64_t za = cell_start(jz, nz, tz), zb = cell_start(jz + 1, nz, tz);
+    uint64_t acc = 0;
+    for (int64_t z = za; z < zb; z++)
+      for (int64_t y = ya; y < yb; y++) {
+        const uint8_t* row = in + (z * ny + y) * nx;
+        uint32_t rs = 0;
+        for (int64_t x = xa; x < xb; x++) rs += __ldg(row + x);
+        acc += rs;
+      }
+    const uint64_t cnt = (uint64_t)(xb - xa) * (uint64_t)(yb - ya) * (uint64_t)(zb - za);
+    out[o] = (uint8_t)((2 * acc + cnt) / (2 * cnt));  // volume.py:306-308 round half up
+  }
+}
+
+// one thread per 4 atlas bytes (or per byte when s % 4 != 0)
+__global__ void encode_atlas_kernel(const uint8_t* __restrict__ cube, int64_t nz, int64_t ny, int64_t nx, int s,
+                                    int grid, int atlas_dim, int map_count, uint8_t* __restrict__ atlases) {
+  const int64_t map_bytes = (int64_t)atlas_dim * atlas_dim;
+  const int64_t total = map_bytes * map_count;
+  const int64_t per = (int64_t)grid * grid;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = o / map_bytes;
+    const int64_t rem = o - m * map_bytes;
+    const int64_t R = rem / atlas_dim, C = rem - (rem / atlas_dim) * atlas_dim;
+    const int64_t cy = R / s, y = R - cy * s;
+    const int64_t cx = C / s, x = C - cx * s;
+    const int64_t k = m * per + cy * grid + cx;
+    uint8_t v = 0;
+    if (k < nz && y < ny && x < nx) v = __ldg(cube + (k * ny + y) * nx + x);
+    atlases[o] = v;
+  }
+}
+
+__global__ void decode_atlas_kernel(const uint8_t* __restrict__ atlases, int s, int grid, int atlas_dim,
+                                    uint8_t* __restrict__ cube) {
+  const int64_t total = (int64_t)s * s * s;
+  const int64_t per = (int64_t)grid * grid;
+  const int64_t map_bytes = (int64_t)atlas_dim * atlas_dim;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = o % s;
+    const int64_t r = o / s;
+    const int64_t y = r % s;
+    const int64_t k = r / s;
+    const int64_t m = k / per, w = k - (k / per) * per;
+    const int64_t cy = w / grid, cx = w - (w / grid) * grid;
+    cube[o] = __ldg(atlases + m * map_bytes + (cy * s + y) * atlas_dim + cx * s + x);
+  }
+}
+
+static int grid1d(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace ctp
+
+using namespace ctp;
+
+extern "C" {
+
+int ctp_downscale_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, int64_t tz, int64_t ty, int64_t tx,
+                     uint8_t* out, void* stream) {
+  CTP_REQUIRE(in && out, CTP_E_INVALID, "ctp_downscale_u8: null pointer");
+  CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1, CTP_E_INVALID, "ctp_downscale_u8: degenerate shape");
+  // volume.py:287-289
+  CTP_REQUIRE(1 <= tx && tx <= nx, CTP_E_INVALID, "target x=%lld outside [1, %lld]", (long long)tx, (long long)nx);
+  CTP_REQUIRE(1 <= ty && ty <= ny, CTP_E_INVALID, "target y=%lld outside [1, %lld]", (long long)ty, (long long)ny);
+  CTP_REQUIRE(1 <= tz && tz <= nz, CTP_E_INVALID, "target z=%lld outside [1, %lld]", (long long)tz, (long long)nz);
+  cudaStream_t st = as_stream(stream);
+  if (tx == nx && ty == ny && tz == nz) {  // volume.py:290-291
+    CTP_CUDA_CALL(cudaMemcpyAsync(out, in, (size_t)(nx * ny * nz), cudaMemcpyDeviceToDevice, st));
+    return CTP_OK;
+  }
+  const int64_t total = tx * ty * tz;
+  downscale_u8_kernel<<<grid1d(total, 256), 256, 0, st>>>(in, nz, ny, nx, tz, ty, tx, out);
+  CTP_CUDA_CHECK_LAUNCH("downscale_u8_kernel");
+  return CTP_OK;
+}
+
+int ctp_encode_atlas_u8(const uint8_t* cube, int64_t nz, int64_t ny, int64_t nx, int32_t s, int32_t grid,
+                        int32_t atlas_dim, int32_t map_count, uint8_t* atlases, void* stream) {
+  CTP_REQUIRE(cube && atlases, CTP_E_INVALID, "ctp_encode_atlas_u8: null pointer");
+  ctp_level_out lo{atlases, CTP_LAYOUT_ATLAS, s, grid, atlas_dim, map_count, 0};
+  int rc = check_level_desc(lo, nx, ny, nz, 0);
+  if (rc != CTP_OK) return rc;
+  const int64_t total = (int64_t)atlas_dim * atlas_dim * map_count;
+  encode_atlas_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(cube, nz, ny, nx, s, grid, atlas_dim,
+                                                                         map_count, atlases);
+  CTP_CUDA_CHECK_LAUNCH("encode_atlas_kernel");
+  return CTP_OK;
+}
+
+int ctp_decode_atlas_u8(const uint8_t* atlases, int32_t s, int32_t grid, int32_t atlas_dim, int32_t map_count,
+                        uint8_t* cube, void* stream) {
+  CTP_REQUIRE(cube && atlases, CTP_E_INVALID, "ctp_decode_atlas_u8: null pointer");
+  ctp_level_out lo{const_cast<uint8_t*>(atlases), CTP_LAYOUT_ATLAS, s, grid, atlas_dim, map_count, 0};
+  int rc = check_level_desc(lo, s, s, s, 0);
+  if (rc != CTP_OK) return rc;
+  const int64_t total = (int64_t)s * s * s;
+  decode_atlas_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(atlases, s, grid, atlas_dim, cube);
+  CTP_CUDA_CHECK_LAUNCH("decode_atlas_kernel");
+  return CTP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,292 @@
+"""Host-array drop-ins for the reference's hot-path entry points.
+
+Same names, signatures, validation order and error classes as the reference
+(ctprev/__init__.py:29-88 re-exports); numpy in, fresh numpy out, with the
+H2D / D2H copies inside and the arithmetic in the sm_100a kernels.
+
+    volume_histogram       volume.py:252-262
+    Histogram256.of        volume.py:117-122
+    artifact_bins          mask.py:215-231
+    filter_histogram_bins  mask.py:234-246
+    downscale_volume       volume.py:277-309
+    encode_slicemaps       slicemap.py:120-142
+    decode_slicemaps       slicemap.py:145-155
+    render_view            render.py:205-236
+    image_entropy          render.py:248-262
+    optimal_snapshot       render.py:273-314
+
+plus the fused ``preview_pipeline`` (one HBM pass for hist + filter + levels
++ atlases) and ``render_views`` (batched, incl. the MIP / alpha extensions).
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as dev
+from .device import AtlasSpec
+from .errors import InvalidTarget, RangeOutOfBounds, UnsupportedPixelFormat, DimensionMismatch
+from .pipeline import plan_preview, run_preview
+from .types import FACTORY, ViewParams, plan_scheme
+
+__all__ = [
+    "volume_histogram", "histogram_of", "artifact_bins", "filter_histogram_bins", "downscale_volume",
+    "encode_slicemaps", "decode_slicemaps", "render_view", "render_views", "image_entropy",
+    "optimal_snapshot", "preview_pipeline", "PreviewResult", "to_device", "cuda_device",
+]
+
+
+def cuda_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.NativeUnavailable("no CUDA device visible: the B200 path has no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(arr: np.ndarray) -> torch.Tensor:
+    """H2D of a host array (read-only numpy arrays are fine: the copy never writes)."""
+    dev_ = cuda_device()
+    a = np.ascontiguousarray(arr)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)  # non-writable numpy -> torch view
+        t = torch.from_numpy(a)
+    return t.to(dev_, non_blocking=False)
+
+
+def _host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def _voxels(volume) -> np.ndarray:
+    return volume.voxels
+
+
+# ---------------------------------------------------------------------------
+# histogram / filter
+
+def histogram_of(values: np.ndarray, cls=None):
+    """Histogram256.of (volume.py:117-122) of any uint8 array."""
+    cls = cls or FACTORY.Histogram256
+    if values.dtype != np.uint8:
+        raise UnsupportedPixelFormat(f"expected uint8 values, got {values.dtype}")
+    flat = np.ascontiguousarray(values).reshape(1, 1, -1) if values.size else None
+    if flat is None:
+        return cls(np.zeros(256, dtype=np.int64))
+    h = dev.hist_u8(to_device(flat))
+    return cls(_host(h))
+
+
+def volume_histogram(volume, z_range: tuple[int, int] | None = None):
+    """volume.py:252-262."""
+    vox = _voxels(volume)
+    if z_range is None:
+        return FACTORY.Histogram256(_host(dev.hist_u8(to_device(vox))))
+    z0, z1 = z_range
+    if not (0 <= z0 < z1 <= vox.shape[0]):
+        raise RangeOutOfBounds(f"z_range {z_range} outside [0, {vox.shape[0]}]")
+    # only the slab crosses PCIe
+    return FACTORY.Histogram256(_host(dev.hist_u8(to_device(vox[z0:z1]))))
+
+
+def artifact_bins(volume, n_top: int = 3, frac: float = 0.0005) -> frozenset:
+    """mask.py:215-231: the top-slab histogram and the cutoff test on the GPU."""
+    vox = _voxels(volume)
+    nz = vox.shape[0]
+    if not 1 <= n_top <= nz:
+        raise RangeOutOfBounds(f"n_top {n_top} outside [1, {nz}]")
+    if frac < 0:
+        raise RangeOutOfBounds(f"frac {frac} must be non-negative")
+    top = to_device(vox[nz - n_top:])
+    th = dev.hist_u8(top)
+    _, flags = dev.lut_from_hist(th, top.numel(), frac, 0)
+    f = _host(flags)
+    return frozenset(int(b) for b in np.nonzero(f)[0])
+
+
+def _lut_from_bins(bins) -> np.ndarray:
+    lut = np.arange(256, dtype=np.uint8)  # mask.py:241-245
+    for b in bins:
+        if not 0 <= int(b) <= 255:
+            raise RangeOutOfBounds(f"bin {b} outside [0, 255]")
+        lut[int(b)] = 0
+    return lut
+
+
+def filter_histogram_bins(volume, bins):
+    """mask.py:234-246: one pass of the LUT kernel."""
+    lut = _lut_from_bins(bins)
+    vox = _voxels(volume)
+    out = dev.lut_apply_u8(to_device(vox), to_device(lut))
+    return FACTORY.Volume(_host(out), getattr(volume, "voxel_size_um", None))
+
+
+# ---------------------------------------------------------------------------
+# downscale / slicemaps
+
+def _check_target(target, dims):
+    tx, ty, tz = (int(t) for t in target)
+    nx, ny, nz = dims
+    for t, n, ax in ((tx, nx, "x"), (ty, ny, "y"), (tz, nz, "z")):  # volume.py:287-289
+        if not 1 <= t <= n:
+            raise InvalidTarget(f"target {ax}={t} outside [1, {n}]")
+    return tx, ty, tz
+
+
+def downscale_volume(volume, target):
+    """volume.py:277-309 (identity returns the same voxels, volume.py:290-291)."""
+    vox = _voxels(volume)
+    nz, ny, nx = vox.shape
+    tx, ty, tz = _check_target(target, (nx, ny, nz))
+    vs = getattr(volume, "voxel_size_um", None)
+    if (tx, ty, tz) == (nx, ny, nz):
+        return FACTORY.Volume(vox, vs)
+    return FACTORY.Volume(_host(_downscale_dev(to_device(vox), (tx, ty, tz))), vs)
+
+
+def _downscale_dev(t: torch.Tensor, target) -> torch.Tensor:
+    """Power-of-two ratios go through the fused pyramid kernel, others the general one."""
+    from .pipeline import level_for_target
+    nz, ny, nx = t.shape
+    l = level_for_target((nz, ny, nx), target) if nx % 16 == 0 else None
+    if l is not None and l >= 1:
+        return dev.preview(t, None, {l: "xyz"})[l]
+    return dev.downscale(t, target)
+
+
+def encode_slicemaps(volume, scheme):
+    """slicemap.py:120-142: downscale to s^3 (errors propagate), then pack."""
+    if isinstance(scheme, int):
+        scheme = plan_scheme(scheme)
+    s = scheme.s
+    vox = _voxels(volume)
+    nz, ny, nx = vox.shape
+    _check_target((s, s, s), (nx, ny, nz))  # slicemap.py:130 -> volume.py:287-289
+    spec = AtlasSpec.of(scheme)
+    t = to_device(vox)
+    cube = t if (nx, ny, nz) == (s, s, s) else _downscale_dev(t, (s, s, s))
+    atl = _host(dev.encode_atlas(cube, spec))
+    return FACTORY.SlicemapSet(scheme=scheme, atlases=tuple(atl[m] for m in range(spec.map_count)))
+
+
+def decode_slicemaps(sset):
+    """slicemap.py:145-155."""
+    sc = sset.scheme
+    spec = AtlasSpec.of(sc)
+    atl = to_device(np.stack([np.asarray(a) for a in sset.atlases]))
+    return FACTORY.Volume(_host(dev.decode_atlas(atl, spec)))
+
+
+# ---------------------------------------------------------------------------
+# rendering
+
+def _view_of(params) -> ViewParams:
+    if isinstance(params, ViewParams):
+        return params
+    return ViewParams(azimuth_deg=params.azimuth_deg, image_dim=params.image_dim, steps=params.steps,
+                      mode=params.mode, threshold=params.threshold, gain=params.gain)
+
+
+def render_view(volume, params) -> np.ndarray:
+    """render.py:205-236 (fp64, bit-identical to the numba kernels)."""
+    p = _view_of(params)
+    img = dev.render(to_device(_voxels(volume)), [p], channels=4 if p.mode == "alpha" else 1)
+    return _host(img[0])
+
+
+def render_views(volume, params_list, channels: int = 1, fp32: bool = False) -> np.ndarray:
+    """Batched views of one volume in one launch (per 64 views)."""
+    ps = [_view_of(p) for p in params_list]
+    return _host(dev.render(to_device(_voxels(volume)), ps, channels=channels, fp32=fp32))
+
+
+def _entropy_from_counts(counts: np.ndarray, size: int):
+    """render.py:256-262 on a histogram (same numpy operations, same bits)."""
+    p = counts / size
+    nzp = p[p > 0]
+    entropy = float(-(nzp * np.log2(nzp)).sum())
+    if entropy == 0.0:
+        entropy = 0.0
+    return entropy, p
+
+
+def image_entropy(image: np.ndarray):
+    """render.py:248-262: histogram on the GPU, the 256-term sum on the host."""
+    if image.ndim != 2 or image.dtype != np.uint8:
+        raise RangeOutOfBounds("entropy expects a 2-d uint8 image")
+    counts = _host(dev.image_hist(to_device(image[None])))[0]
+    h, p = _entropy_from_counts(counts, image.size)
+    return FACTORY.EntropyResult(entropy=h, probabilities=p)
+
+
+def optimal_snapshot(volume, n_views: int = 36, params=None):
+    """render.py:273-314: all views rendered in one batched launch, per-view
+    histograms on the device, the argmax (strict '>', smallest azimuth wins) on the host."""
+    if n_views < 1:
+        raise RangeOutOfBounds(f"n_views {n_views} must be positive")
+    template = _view_of(params) if params is not None else ViewParams()
+    step = 360.0 / n_views
+    views = [ViewParams(azimuth_deg=k * step, image_dim=template.image_dim, steps=template.steps,
+                        mode=template.mode, threshold=template.threshold, gain=template.gain)
+             for k in range(n_views)]
+    vol_t = to_device(_voxels(volume))
+    imgs = dev.render(vol_t, views, channels=1)
+    counts = _host(dev.image_hist(imgs))
+    size = template.image_dim * template.image_dim
+    best_k, best_h, per_view = 0, -1.0, []
+    for k in range(n_views):
+        h, _ = _entropy_from_counts(counts[k], size)
+        per_view.append((k * step, h))
+        if h > best_h:
+            best_k, best_h = k, h
+    return FACTORY.SnapshotResult(azimuth_deg=best_k * step, image=_host(imgs[best_k]), entropy=best_h,
+                                  per_view=tuple(per_view))
+
+
+# ---------------------------------------------------------------------------
+# fused pipeline
+
+@dataclass
+class PreviewResult:
+    histogram: np.ndarray          # int64[256] (u8) or int64[4096] (u16)
+    bins: frozenset                # artifact bins (incl. 0)
+    slicemaps: dict                # s -> SlicemapSet
+    levels: dict                   # s -> Volume (only when materialised)
+    filtered: object | None        # Volume of the filtered (and rescaled) full-res voxels, if kept
+
+
+def preview_pipeline(volume, schemes=(512, 256, 128), n_top: int = 3, frac: float = 0.0005,
+                     keep_filtered: bool = False) -> PreviewResult:
+    """hist + artifact bins + filter (+ 16->8 rescale for uint16) + per-scheme
+    levels (direct from the filtered volume) + atlases in one device pass.
+
+    ``volume``: a Volume, or a (nz, ny, nx) uint8 / uint16 (12-bit) array.
+    ``schemes``: iterable of ints (plan_scheme) or SlicemapScheme objects."""
+    vox = volume if isinstance(volume, np.ndarray) else _voxels(volume)
+    if vox.ndim != 3 or min(vox.shape) < 1:
+        raise DimensionMismatch("voxels must be a 3-d array (nz, ny, nx)")
+    if vox.dtype not in (np.uint8, np.uint16):
+        raise UnsupportedPixelFormat(f"voxels must be uint8 or uint16, got {vox.dtype}")
+    nz = vox.shape[0]
+    if not 1 <= n_top <= nz:
+        raise RangeOutOfBounds(f"n_top {n_top} outside [1, {nz}]")
+    if frac < 0:
+        raise RangeOutOfBounds(f"frac {frac} must be non-negative")
+    sch = {}
+    for sc in schemes:
+        sc = plan_scheme(sc) if isinstance(sc, int) else sc
+        sch[sc.s] = sc
+    plan = plan_preview(vox.shape, {s: AtlasSpec.of(sc) for s, sc in sch.items()}, keep_filtered=keep_filtered)
+    res = run_preview(to_device(vox), plan, n_top, frac)
+    slicemaps = {}
+    for s, sc in sch.items():
+        a = _host(res.atlases[s])
+        slicemaps[s] = FACTORY.SlicemapSet(scheme=sc, atlases=tuple(a[m] for m in range(sc.map_count)))
+    levels = {s: FACTORY.Volume(_host(t)) for s, t in res.levels.items()}
+    flags = _host(res.flags)
+    filtered = FACTORY.Volume(_host(res.filtered)) if (keep_filtered and res.filtered is not None) else None
+    return PreviewResult(_host(res.hist), frozenset(int(b) for b in np.nonzero(flags)[0]), slicemaps, levels,
+                         filtered)

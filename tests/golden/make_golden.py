@@ -1,0 +1,142 @@
+"""Generate the golden fixtures by running the REFERENCE itself (ctprev).
+
+Run in the builder container, where /root/reference exists:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/ref_golden.npz (committed).  The GPU box never reads
+/root/reference: tests compare the CPU oracle and the CUDA path against these
+frozen reference outputs.
+"""
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_ctprev")
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+from ctprev.mask import artifact_bins, filter_histogram_bins  # noqa: E402
+from ctprev.phantom import BoxSpec, CylinderSpec, PhantomSpec, SphereSpec, generate_phantom  # noqa: E402
+from ctprev.render import ADDITIVE, SURFACE, ViewParams, image_entropy, optimal_snapshot, render_view  # noqa: E402
+from ctprev.slicemap import SlicemapScheme, encode_slicemaps, plan_scheme  # noqa: E402
+from ctprev.volume import Volume, downscale_volume, volume_histogram  # noqa: E402
+
+OUT = Path(__file__).resolve().parent / "ref_golden.npz"
+
+
+def main() -> None:
+    g: dict[str, np.ndarray] = {}
+    rng = np.random.default_rng(20231115)
+
+    # ---- histogram (volume.py:252-262), incl. degenerate and ragged shapes
+    hist_cases = [((1, 1, 1), None), ((3, 5, 7), None), ((7, 9, 33), (2, 5)), ((16, 24, 32), (0, 16)),
+                  ((16, 24, 32), (15, 16)), ((5, 16, 48), (1, 4))]
+    for i, (shape, zr) in enumerate(hist_cases):
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        g[f"hist{i}_in"] = v
+        g[f"hist{i}_z"] = np.array(zr if zr else (-1, -1), dtype=np.int64)
+        g[f"hist{i}_out"] = volume_histogram(Volume(v), zr).bins.copy()
+    g["hist_n"] = np.array(len(hist_cases))
+
+    # ---- artifact bins + filter (mask.py:215-246)
+    vox = np.zeros((8, 64, 64), dtype=np.uint8)       # the reference's own test stack (test_mask.py:155-161)
+    vox[:6] = 90
+    vox[6:] = 140
+    vox[6:, :8, :8] = 200
+    vox[7, 30, 30] = 90
+    art_cases = [(vox, 2, 0.0005), (vox, 3, 0.0005), (vox, 1, 0.01)]
+    for n_top, frac in ((3, 0.0005), (2, 0.002), (1, 0.0)):
+        bg = np.clip(np.rint(rng.normal(20, 6, size=(12, 40, 48))), 0, 255).astype(np.uint8)
+        art_cases.append((bg, n_top, frac))
+    for i, (v, n_top, frac) in enumerate(art_cases):
+        bins = artifact_bins(Volume(v), n_top=n_top, frac=frac)
+        g[f"art{i}_in"] = v
+        g[f"art{i}_ntop"] = np.array(n_top)
+        g[f"art{i}_frac"] = np.array(frac)
+        g[f"art{i}_bins"] = np.array(sorted(bins), dtype=np.int64)
+        g[f"art{i}_filtered"] = filter_histogram_bins(Volume(v), bins).voxels.copy()
+    g["art_n"] = np.array(len(art_cases))
+
+    # ---- downscale (volume.py:265-309) incl. non-integer ratios
+    ds_cases = [((8, 8, 8), (4, 4, 4)), ((16, 16, 10), (4, 16, 16)), ((19, 23, 37), (5, 7, 3)),
+                ((24, 40, 40), (32, 32, 20)), ((32, 32, 32), (4, 4, 4)), ((12, 12, 12), (12, 12, 12)),
+                ((9, 17, 33), (1, 1, 1)), ((64, 48, 48), (24, 24, 32)), ((16, 32, 64), (16, 8, 4))]
+    for i, (shape, target) in enumerate(ds_cases):
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        g[f"ds{i}_in"] = v
+        g[f"ds{i}_target"] = np.array(target, dtype=np.int64)
+        g[f"ds{i}_out"] = downscale_volume(Volume(v), target).voxels.copy()
+    g["ds_n"] = np.array(len(ds_cases))
+
+    # ---- slicemaps (slicemap.py:120-142), custom + planned schemes
+    enc_cases = [((64, 64, 64), (64, 512, 8, 1)), ((96, 96, 96), (96, 768, 8, 2)), ((100, 90, 80), (64, 512, 8, 1)),
+                 ((32, 32, 32), (32, 128, 4, 2)), ((48, 64, 64), (48, 384, 8, 1)), ((128, 128, 128), 128)]
+    for i, (shape, sc) in enumerate(enc_cases):
+        if isinstance(sc, int):
+            zs = np.arange(shape[0]).reshape(-1, 1, 1)
+            ys = np.arange(shape[1]).reshape(1, -1, 1)
+            xs = np.arange(shape[2]).reshape(1, 1, -1)
+            v = ((zs * 7 + ys * 3 + xs * 31) % 256).astype(np.uint8)
+            scheme = plan_scheme(sc)
+        else:
+            v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+            scheme = SlicemapScheme(*sc)
+        sset = encode_slicemaps(Volume(v), scheme)
+        g[f"enc{i}_in"] = v
+        g[f"enc{i}_scheme"] = np.array([scheme.s, scheme.atlas_dim, scheme.grid, scheme.map_count], dtype=np.int64)
+        g[f"enc{i}_out"] = np.stack(sset.atlases)
+    g["enc_n"] = np.array(len(enc_cases))
+
+    # ---- render (render.py:205-236): L-phantom (test_render.py:36-48) and a sphere
+    l_ph = generate_phantom(PhantomSpec(
+        dims=(96, 96, 96),
+        objects=(BoxSpec((8, 40, 8), (88, 56, 24), value=(150, 150)),
+                 BoxSpec((8, 40, 24), (24, 56, 88), value=(220, 220)),
+                 SphereSpec(70.0, 48.0, 60.0, r=10.0, value=(90, 90))),
+        seed=4)).volume
+    g["lphantom"] = l_ph.voxels.copy()
+    cyl = generate_phantom(PhantomSpec(
+        dims=(96, 96, 96),
+        container=CylinderSpec(cx=47.5, cy=47.5, r=36.0, wall=36.0, value=(180, 180)), seed=3)).volume
+    g["cylinder"] = cyl.voxels.copy()
+    aniso = rng.integers(0, 256, size=(20, 28, 36), dtype=np.uint8)
+    g["aniso"] = aniso
+    rcases = [("lphantom", 17.0, 64, 64, SURFACE, 60), ("lphantom", 0.0, 48, 96, ADDITIVE, 1),
+              ("lphantom", 123.4, 64, 64, SURFACE, 1), ("lphantom", 300.0, 32, 128, ADDITIVE, 1),
+              ("aniso", 45.0, 32, 64, SURFACE, 100), ("aniso", 200.0, 32, 64, ADDITIVE, 1),
+              ("cylinder", 90.0, 40, 40, SURFACE, 60)]
+    vols = {"lphantom": l_ph, "cylinder": cyl, "aniso": Volume(aniso)}
+    for i, (name, az, dim, steps, mode, thr) in enumerate(rcases):
+        img = render_view(vols[name], ViewParams(azimuth_deg=az, image_dim=dim, steps=steps, mode=mode,
+                                                 threshold=thr))
+        g[f"rv{i}_vol"] = np.frombuffer(name.encode(), dtype=np.uint8)
+        g[f"rv{i}_params"] = np.array([az, dim, steps, 1.0 if mode == ADDITIVE else 0.0, thr], dtype=np.float64)
+        g[f"rv{i}_out"] = img
+    g["rv_n"] = np.array(len(rcases))
+
+    # ---- entropy + snapshot (render.py:248-314); test_render.py:170-179 known answer
+    snap = optimal_snapshot(l_ph, n_views=12, params=ViewParams(image_dim=128, steps=64, threshold=60))
+    g["snap_az"] = np.array(snap.azimuth_deg)
+    g["snap_h"] = np.array(snap.entropy)
+    g["snap_per_view"] = np.array(snap.per_view, dtype=np.float64)
+    g["snap_img"] = snap.image
+    ent_imgs = [np.full((64, 64), 7, np.uint8), np.tile(np.arange(256, dtype=np.uint8), 256).reshape(256, 256),
+                rng.integers(0, 256, size=(32, 32), dtype=np.uint8), snap.image]
+    for i, im in enumerate(ent_imgs):
+        g[f"ent{i}_in"] = im
+        g[f"ent{i}_h"] = np.array(image_entropy(im).entropy)
+    g["ent_n"] = np.array(len(ent_imgs))
+
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB, {len(g)} arrays)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,252 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Bit-exact for histograms, bins, filtered voxels,
+levels, atlases and the fp64 reference render modes; MIP / alpha (fp32
+extension path) within max-abs 1 (= 1/255) per channel."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ctp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P(cuda):
+    import paper_2311_15038_b200 as P
+    return P
+
+
+# ---------------------------------------------------------------- golden (reference outputs)
+
+def test_hist_golden(P, golden):
+    for i in range(int(golden["hist_n"])):
+        zr = tuple(int(x) for x in golden[f"hist{i}_z"])
+        zr = None if zr == (-1, -1) else zr
+        h = P.volume_histogram(P.Volume(golden[f"hist{i}_in"]), zr)
+        assert h.bins.dtype == np.int64 and np.array_equal(h.bins, golden[f"hist{i}_out"]), i
+
+
+def test_artifact_filter_golden(P, golden):
+    for i in range(int(golden["art_n"])):
+        v = P.Volume(golden[f"art{i}_in"])
+        bins = P.artifact_bins(v, n_top=int(golden[f"art{i}_ntop"]), frac=float(golden[f"art{i}_frac"]))
+        assert sorted(bins) == golden[f"art{i}_bins"].tolist(), i
+        assert np.array_equal(P.filter_histogram_bins(v, bins).voxels, golden[f"art{i}_filtered"]), i
+
+
+def test_downscale_golden(P, golden):
+    for i in range(int(golden["ds_n"])):
+        out = P.downscale_volume(P.Volume(golden[f"ds{i}_in"]), tuple(int(t) for t in golden[f"ds{i}_target"]))
+        assert np.array_equal(out.voxels, golden[f"ds{i}_out"]), i
+
+
+def test_encode_golden(P, golden):
+    for i in range(int(golden["enc_n"])):
+        s, a, g, m = (int(x) for x in golden[f"enc{i}_scheme"])
+        sset = P.encode_slicemaps(P.Volume(golden[f"enc{i}_in"]), P.SlicemapScheme(s, a, g, m))
+        assert np.array_equal(np.stack(sset.atlases), golden[f"enc{i}_out"]), i
+        back = P.decode_slicemaps(sset)
+        assert np.array_equal(np.stack(P.encode_slicemaps(back, sset.scheme).atlases), golden[f"enc{i}_out"])
+
+
+def test_render_golden_bit_exact(P, golden):
+    for i in range(int(golden["rv_n"])):
+        az, dim, steps, add, thr = golden[f"rv{i}_params"]
+        vol = P.Volume(golden[bytes(golden[f"rv{i}_vol"]).decode()])
+        img = P.render_view(vol, P.ViewParams(azimuth_deg=az, image_dim=int(dim), steps=int(steps),
+                                              mode="additive" if add else "surface", threshold=int(thr)))
+        assert img.shape == (int(dim), int(dim)) and img.dtype == np.uint8
+        assert np.array_equal(img, golden[f"rv{i}_out"]), (i, int(np.abs(img.astype(int) - golden[f"rv{i}_out"]).max()))
+
+
+def test_entropy_and_snapshot_golden(P, golden):
+    for i in range(int(golden["ent_n"])):
+        assert P.image_entropy(golden[f"ent{i}_in"]).entropy == float(golden[f"ent{i}_h"])
+    snap = P.optimal_snapshot(P.Volume(golden["lphantom"]), n_views=12,
+                              params=P.ViewParams(image_dim=128, steps=64, threshold=60))
+    assert snap.azimuth_deg == 300.0 == float(golden["snap_az"])       # test_render.py:178
+    assert snap.entropy == float(golden["snap_h"])                       # bit-identical H
+    assert np.array_equal(np.array(snap.per_view), golden["snap_per_view"])
+    assert np.array_equal(snap.image, golden["snap_img"])
+
+
+def test_symmetric_cylinder_reports_zero(P, golden):
+    snap = P.optimal_snapshot(P.Volume(golden["cylinder"]), n_views=4,
+                              params=P.ViewParams(image_dim=128, steps=64, threshold=60))
+    ents = [h for _, h in snap.per_view]
+    assert max(ents) - min(ents) <= 1e-6 and snap.azimuth_deg == 0.0    # test_render.py:181-193
+
+
+# ---------------------------------------------------------------- oracle, seeded inputs
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 5), (17, 33, 65), (64, 64, 64), (3, 1000, 1001)])
+def test_hist_random(P, shape):
+    rng = np.random.default_rng(sum(shape))
+    v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+    assert np.array_equal(P.volume_histogram(P.Volume(v)).bins, O.histogram(v))
+    if shape[0] > 2:
+        assert np.array_equal(P.volume_histogram(P.Volume(v), (1, shape[0] - 1)).bins, O.histogram(v, (1, shape[0] - 1)))
+
+
+def test_hist_skewed_and_constant(P):
+    for v in (np.full((32, 64, 64), 7, np.uint8),
+              np.clip(np.rint(np.random.default_rng(1).normal(20, 6, (40, 96, 96))), 0, 255).astype(np.uint8)):
+        assert np.array_equal(P.volume_histogram(P.Volume(v)).bins, O.histogram(v))
+
+
+def test_hist_u16_device(P, cuda):
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(3)
+    v = rng.integers(0, 5000, size=(9, 31, 77)).astype(np.uint16)
+    h = dev.hist_u16(torch.from_numpy(v).to(cuda)).cpu().numpy()
+    assert np.array_equal(h, O.histogram_u16(v))
+
+
+def test_filter_unaligned_lengths(P):
+    rng = np.random.default_rng(4)
+    for shape in [(1, 1, 17), (3, 7, 11), (5, 64, 65)]:
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        bins = {0, 3, 77, 255}
+        assert np.array_equal(P.filter_histogram_bins(P.Volume(v), bins).voxels, O.filter_histogram_bins(v, bins))
+
+
+def test_downscale_random_ratios(P):
+    rng = np.random.default_rng(5)
+    for shape, target in [((30, 40, 50), (25, 20, 15)), ((64, 64, 64), (32, 32, 32)), ((64, 64, 64), (8, 8, 8)),
+                          ((32, 48, 64), (4, 3, 2)), ((96, 160, 160), (128, 128, 96)), ((33, 17, 9), (9, 17, 33))]:
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        assert np.array_equal(P.downscale_volume(P.Volume(v), target).voxels, O.downscale(v, target)), (shape, target)
+
+
+def test_errors_match_reference(P):
+    v = P.Volume(np.zeros((4, 4, 4), np.uint8))
+    with pytest.raises(P.InvalidTarget):
+        P.downscale_volume(v, (4, 4, 8))
+    with pytest.raises(P.InvalidTarget):
+        P.downscale_volume(v, (0, 4, 4))
+    with pytest.raises(P.RangeOutOfBounds):
+        P.volume_histogram(v, (2, 2))
+    with pytest.raises(P.RangeOutOfBounds):
+        P.artifact_bins(v, n_top=0)
+    with pytest.raises(P.RangeOutOfBounds):
+        P.artifact_bins(v, frac=-0.1)
+    with pytest.raises(P.RangeOutOfBounds):
+        P.filter_histogram_bins(v, {256})
+    with pytest.raises(P.InvalidTarget):
+        P.encode_slicemaps(v, 128)      # smaller than the scheme (slicemap.py:130)
+    with pytest.raises(P.UnsupportedScheme):
+        P.encode_slicemaps(v, 100)
+    with pytest.raises(P.RangeOutOfBounds):
+        P.image_entropy(np.zeros((4, 4, 4), np.uint8))
+    with pytest.raises(P.RangeOutOfBounds):
+        P.optimal_snapshot(v, n_views=0)
+
+
+# ---------------------------------------------------------------- fused pipeline (kernels 1-4)
+
+def _synth_host(spec):
+    from paper_2311_15038_b200 import synth
+    return synth.generate(spec).cpu().numpy()
+
+
+def _check_preview(P, vox, schemes, keep_filtered=False):
+    res = P.preview_pipeline(vox, schemes=schemes, keep_filtered=keep_filtered)
+    sch = [(sc.s, sc.atlas_dim, sc.grid, sc.map_count) if not isinstance(sc, int) else O.plan_scheme(sc)
+           for sc in schemes]
+    hist, bins, f, levels, atl = O.preview_pipeline(vox, [s[0] for s in sch], schemes=sch)
+    assert np.array_equal(res.histogram, hist)
+    assert res.bins == bins
+    for s, a in zip(sch, atl):
+        got = np.stack(res.slicemaps[s[0]].atlases)
+        assert np.array_equal(got, np.stack(a)), s
+    if keep_filtered:
+        assert np.array_equal(res.filtered.voxels, f)
+    return res
+
+
+def test_preview_c1_full_size(P):
+    """Config 1 exactly: 256^3 u8 seed 0, 3 shells; one 16x16-grid 4096^2 atlas."""
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.config("c1"))
+    _check_preview(P, vox, [P.SlicemapScheme(256, 4096, 16, 1)], keep_filtered=True)
+
+
+def test_preview_four_levels_512(P):
+    """Levels 1..4 of a 512^3 volume (planned 256/128 + custom 64/32 schemes) in one pass."""
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.small((512, 512, 512), seed=7, n_shells=6))
+    _check_preview(P, vox, [256, 128, P.SlicemapScheme(64, 512, 8, 1), P.SlicemapScheme(32, 256, 8, 1)])
+
+
+def test_preview_anisotropic_and_general(P):
+    """Non-cubic: power-of-two levels fused; a 1.5:1 level via the general path; padding."""
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.small((96, 192, 160), seed=8))       # nz, ny, nx
+    _check_preview(P, vox, [128, P.SlicemapScheme(96, 768, 8, 2), P.SlicemapScheme(48, 384, 8, 1)],
+                   keep_filtered=True)
+
+
+def test_preview_u16_extension(P):
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.small((64, 128, 128), dtype="u16", seed=9))
+    res = _check_preview(P, vox, [128, P.SlicemapScheme(64, 512, 8, 1), P.SlicemapScheme(32, 256, 8, 1)],
+                         keep_filtered=True)
+    assert res.histogram.shape == (4096,)
+
+
+def test_preview_c2_full_size(P):
+    """Config 2 exactly (1024^3 u8, 12 shells, 1% speckle): hist, bins and all three
+    levels' atlases bit-exact against the oracle composition."""
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.config("c2"))
+    _check_preview(P, vox, [512, 256, 128])
+
+
+def test_preview_repeat_bit_identical(P):
+    from paper_2311_15038_b200 import synth
+    vox = _synth_host(synth.small((128, 128, 128), seed=10))
+    a = P.preview_pipeline(vox, schemes=[128, P.SlicemapScheme(64, 512, 8, 1)])
+    b = P.preview_pipeline(vox, schemes=[128, P.SlicemapScheme(64, 512, 8, 1)])
+    assert np.array_equal(a.histogram, b.histogram)
+    for s in (128, 64):
+        assert np.array_equal(np.stack(a.slicemaps[s].atlases), np.stack(b.slicemaps[s].atlases))
+
+
+# ---------------------------------------------------------------- renderer extensions
+
+TF = ((0.0, 0.0, 0.0, 0.0, 0.0), (40.0, 0.9, 0.2, 0.1, 0.02), (150.0, 1.0, 0.8, 0.5, 0.08),
+      (255.0, 1.0, 1.0, 1.0, 0.5))
+
+
+def test_mip_fp64_exact_and_fp32_within_one(P, golden):
+    vol = golden["lphantom"]
+    for az in (0.0, 33.0, 250.0):
+        ref = O.render_mip(vol, az, 64, 96)
+        p = P.ViewParams(azimuth_deg=az, image_dim=64, steps=96, mode="mip")
+        g64 = P.render_views(P.Volume(vol), [p], channels=1, fp32=False)[0]
+        g32 = P.render_views(P.Volume(vol), [p], channels=1, fp32=True)[0]
+        assert np.array_equal(g64, ref)
+        assert int(np.abs(g32.astype(int) - ref).max()) <= 1
+
+
+def test_alpha_fp64_and_fp32_within_one(P):
+    rng = np.random.default_rng(11)
+    vol = np.clip(np.rint(rng.normal(60, 40, (40, 48, 56))), 0, 255).astype(np.uint8)
+    for az in (10.0, 135.0):
+        ref = O.render_alpha(vol, az, 48, 80, TF, 0.99)
+        p = P.ViewParams(azimuth_deg=az, image_dim=48, steps=80, mode="alpha", tf=TF)
+        g64 = P.render_views(P.Volume(vol), [p], channels=4, fp32=False)[0]
+        g32 = P.render_views(P.Volume(vol), [p], channels=4, fp32=True)[0]
+        assert np.array_equal(g64, ref)
+        assert int(np.abs(g32.astype(int) - ref.astype(int)).max()) <= 1
+
+
+def test_batched_views_equal_single_views(P, golden):
+    vol = P.Volume(golden["lphantom"])
+    ps = [P.ViewParams(azimuth_deg=10.0 * k, image_dim=48, steps=64, threshold=60) for k in range(5)]
+    batch = P.render_views(vol, ps)
+    for k, p in enumerate(ps):
+        assert np.array_equal(batch[k], O.render_view(golden["lphantom"], p.azimuth_deg, 48, 64, "surface", 60))

@@ -1,0 +1,183 @@
+"""Pin the CPU oracle before trusting it (CPU only).
+
+1. Against the golden vectors produced by running the reference itself
+   (tests/golden/make_golden.py -> ref_golden.npz).
+2. Against the known answers in the reference's own tests
+   (pkg/tests/test_volume.py, test_mask.py, test_slicemap.py, test_render.py).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ctp_oracle as O
+
+
+# ---------------------------------------------------------------- golden vectors
+
+def test_histogram_golden(golden):
+    for i in range(int(golden["hist_n"])):
+        zr = tuple(int(x) for x in golden[f"hist{i}_z"])
+        zr = None if zr == (-1, -1) else zr
+        assert np.array_equal(O.histogram(golden[f"hist{i}_in"], zr), golden[f"hist{i}_out"])
+
+
+def test_artifact_bins_and_filter_golden(golden):
+    for i in range(int(golden["art_n"])):
+        v = golden[f"art{i}_in"]
+        bins = O.artifact_bins(v, int(golden[f"art{i}_ntop"]), float(golden[f"art{i}_frac"]))
+        assert sorted(bins) == golden[f"art{i}_bins"].tolist()
+        assert np.array_equal(O.filter_histogram_bins(v, bins), golden[f"art{i}_filtered"])
+
+
+def test_downscale_golden(golden):
+    for i in range(int(golden["ds_n"])):
+        out = O.downscale(golden[f"ds{i}_in"], tuple(golden[f"ds{i}_target"]))
+        assert np.array_equal(out, golden[f"ds{i}_out"]), i
+
+
+def test_encode_golden(golden):
+    for i in range(int(golden["enc_n"])):
+        sc = tuple(int(x) for x in golden[f"enc{i}_scheme"])
+        atl = np.stack(O.encode_slicemaps(golden[f"enc{i}_in"], sc))
+        assert np.array_equal(atl, golden[f"enc{i}_out"]), i
+
+
+def _render_vol(golden, i):
+    return golden[bytes(golden[f"rv{i}_vol"]).decode()]
+
+
+def test_render_golden_bit_exact(golden):
+    for i in range(int(golden["rv_n"])):
+        az, dim, steps, add, thr = golden[f"rv{i}_params"]
+        img = O.render_view(_render_vol(golden, i), az, int(dim), int(steps), "additive" if add else "surface",
+                            int(thr))
+        assert np.array_equal(img, golden[f"rv{i}_out"]), i
+
+
+def test_entropy_golden(golden):
+    for i in range(int(golden["ent_n"])):
+        assert O.image_entropy(golden[f"ent{i}_in"])[0] == float(golden[f"ent{i}_h"])
+
+
+def test_snapshot_golden(golden):
+    az, img, h, per_view = O.optimal_snapshot(golden["lphantom"], 12, 128, 64, "surface", 60)
+    assert az == float(golden["snap_az"]) == 300.0           # test_render.py:178
+    assert h == float(golden["snap_h"]) and abs(h - 0.798789) <= 1e-5  # test_render.py:179
+    assert np.array_equal(np.array(per_view), golden["snap_per_view"])
+    assert np.array_equal(img, golden["snap_img"])
+
+
+# ------------------------------------------------ reference tests' known answers
+
+def test_hist_known_answers():
+    data = np.zeros((2, 2, 2), dtype=np.uint8)          # test_volume.py:70-78
+    data.ravel()[:4] = [1, 1, 2, 255]
+    h = O.histogram(data)
+    assert h.sum() == 8 and h[0] == 4 and h[1] == 2 and h[2] == 1 and h[255] == 1
+    data = np.zeros((4, 2, 2), dtype=np.uint8)          # test_volume.py:80-86 (half-open)
+    data[1] = 9
+    data[2] = 9
+    h = O.histogram(data, (1, 3))
+    assert h.sum() == 8 and h[9] == 8
+
+
+def test_artifact_known_answers():
+    vox = np.zeros((8, 64, 64), dtype=np.uint8)         # test_mask.py:155-164
+    vox[:6] = 90
+    vox[6:] = 140
+    vox[6:, :8, :8] = 200
+    vox[7, 30, 30] = 90
+    assert sorted(O.artifact_bins(vox, n_top=2)) == [0, 140, 200]
+    assert 90 not in O.artifact_bins(vox, n_top=2)
+    with pytest.raises(ValueError):
+        O.artifact_bins(vox, n_top=0)
+    with pytest.raises(ValueError):
+        O.artifact_bins(vox, n_top=9)
+
+
+def test_filter_known_answers():
+    vox = np.arange(256, dtype=np.uint8).reshape(1, 16, 16)  # test_mask.py:187-194
+    out = O.filter_histogram_bins(vox, {10, 200})
+    assert out[0, 0, 10] == 0 and out[0, 12, 8] == 0
+    keep = np.ones(256, dtype=bool)
+    keep[[0, 10, 200]] = False
+    assert np.array_equal(out.ravel()[keep], vox.ravel()[keep])
+
+
+def test_downscale_known_answers():
+    rng = np.random.default_rng(2)                      # test_volume.py:200-207
+    data = rng.integers(0, 256, size=(8, 8, 8), dtype=np.uint8)
+    blocks = data.reshape(4, 2, 4, 2, 4, 2).sum(axis=(1, 3, 5), dtype=np.int64)
+    assert np.array_equal(O.downscale(data, (4, 4, 4)), ((2 * blocks + 8) // 16).astype(np.uint8))
+    data = np.arange(10, dtype=np.uint8).reshape(1, 1, 10).repeat(16, axis=0)  # test_volume.py:209-216
+    data = np.ascontiguousarray(data.repeat(16, axis=1))[:16, :16, :]
+    assert O.downscale(data, (4, 16, 16))[0, 0].tolist() == [1, 3, 6, 8]
+    assert O.cell_starts(10, 4).tolist() == [0, 2, 5, 7, 10]
+    v = np.full((7, 9, 11), 137, dtype=np.uint8)       # test_volume.py:218-221
+    assert (O.downscale(v, (3, 4, 5)) == 137).all()
+    two = np.array([0, 0, 0, 0, 255, 255, 255, 255], dtype=np.uint8).reshape(2, 2, 2)
+    assert O.downscale(two, (1, 1, 1))[0, 0, 0] == 128
+
+
+def test_slicemap_known_answers():
+    for s, atlas, maps in ((128, 1024, 2), (256, 2048, 4), (512, 4096, 8)):  # test_slicemap.py:35-41
+        assert O.plan_scheme(s) == (s, atlas, 8, maps)
+    sc = O.plan_scheme(128)                              # test_slicemap.py:88-97
+    vox = np.zeros((128, 128, 128), dtype=np.uint8)
+    vox[77, 13, 101] = 251
+    atl = O.encode_slicemaps(vox, sc)
+    k = 77
+    m, w = divmod(k, 64)
+    cy, cx = divmod(w, 8)
+    assert atl[m][cy * 128 + 13, cx * 128 + 101] == 251
+    assert int(np.count_nonzero(np.stack(atl))) == 1
+    sc96 = (96, 768, 8, 2)                               # test_slicemap.py:110-121
+    v = np.full((96, 96, 96), 9, dtype=np.uint8)
+    atl = O.encode_slicemaps(v, sc96)
+    tail = atl[1].reshape(8, 96, 8, 96).transpose(0, 2, 1, 3).reshape(64, 96, 96)
+    assert (tail[:32] == 9).all() and not tail[32:].any()
+    assert np.array_equal(O.decode_slicemaps(atl, sc96), v)
+    zs = np.arange(512, dtype=np.uint16).reshape(512, 1, 1)  # test_slicemap.py:129-135
+    ys = np.arange(512, dtype=np.uint16).reshape(1, 512, 1)
+    xs = np.arange(512, dtype=np.uint16).reshape(1, 1, 512)
+    v = ((zs * 7 + ys * 3 + xs * 31) % 256).astype(np.uint8)
+    assert np.array_equal(O.decode_slicemaps(O.encode_slicemaps(v, O.plan_scheme(512)), O.plan_scheme(512)), v)
+
+
+def test_entropy_known_answers():
+    assert O.image_entropy(np.full((64, 64), 7, dtype=np.uint8))[0] == 0.0  # test_render.py:140-153
+    h = O.image_entropy(np.full((64, 64), 7, dtype=np.uint8))[0]
+    assert math.copysign(1.0, h) == 1.0
+    img = np.tile(np.arange(256, dtype=np.uint8), 256).reshape(256, 256)
+    assert abs(O.image_entropy(img)[0] - 8.0) <= 1e-9
+    img = np.zeros((64, 64), dtype=np.uint8)
+    img[:32] = 255
+    assert abs(O.image_entropy(img)[0] - 1.0) <= 1e-9
+
+
+def test_sphere_silhouette_known_answer():
+    # test_render.py:77-86 at reduced size (64^3 sphere, 128^2): within 3% of analytic
+    n = 64
+    zz, yy, xx = np.mgrid[0:n, 0:n, 0:n]
+    vox = np.zeros((n, n, n), dtype=np.uint8)
+    c = (n - 1) / 2
+    vox[(xx - c) ** 2 + (yy - c) ** 2 + (zz - c) ** 2 <= 20.0 ** 2] = 200
+    img = O.render_view(vox, 0.0, 128, 128, "surface", 100)
+    r_px = (20.0 / n) * 128 / math.sqrt(3.0)
+    analytic = math.pi * r_px * r_px
+    assert abs(int((img > 0).sum()) - analytic) / analytic <= 0.03
+
+
+def test_extension_rescale_rule():
+    v = np.arange(4096)
+    r = O.rescale_u16_to_u8(v)
+    assert r[0] == 0 and r[4095] == 255 and r.dtype == np.uint8
+    # round half up of v*255/4095, exact in integers
+    exact = np.floor(v * 255 / 4095 + 0.5).astype(np.int64)
+    assert np.array_equal(r.astype(np.int64), exact)
+    assert np.all(np.diff(r.astype(int)) >= 0)
+    lut = O.lut_u16({0, 5, 4095})
+    assert lut[0] == 0 and lut[5] == 0 and lut[4095] == 0 and lut[4094] == r[4094]
