@@ -52,25 +52,34 @@ struct LevelDst {
   uint8_t* out;
   int32_t layout;
   int32_t s, grid, atlas_dim;
+  int32_t gshift;          // log2(grid) when grid is a power of two, else -1
+  int32_t z_off;           // added to the slab-local z: global slice index for atlases, 0 for dense
   int64_t nx, ny;          // level dims (x, y) for the dense layout
   int64_t map_bytes;       // atlas_dim^2
-  int64_t z_off;           // added to the slab-local z: global slice index for atlases, 0 for dense
 };
 
 // Byte offset of level voxel (z, y, x), z slab-local (z_off makes it the
 // global slice index for atlases).  Atlas: slicemap.py:79-85 (slice_cell) and the mosaic of
 // slicemap.py:139-140: atlas[m][cy*s + y, cx*s + x] = cube[m*g^2 + cy*g + cx, y, x].
-__device__ __forceinline__ int64_t level_offset(const LevelDst& d, int64_t z, int64_t y, int64_t x) {
+__device__ __forceinline__ int64_t level_offset(const LevelDst& d, int z, int y, int x) {
   z += d.z_off;
   if (d.layout == CTP_LAYOUT_ATLAS) {
-    int64_t per = (int64_t)d.grid * d.grid;
-    int64_t m = z / per;
-    int64_t w = z - m * per;
-    int64_t cy = w / d.grid;
-    int64_t cx = w - cy * d.grid;
-    return m * d.map_bytes + (cy * d.s + y) * (int64_t)d.atlas_dim + cx * d.s + x;
+    int m, cy, cx;
+    if (d.gshift >= 0) {
+      const int w = z & ((1 << (2 * d.gshift)) - 1);
+      m = z >> (2 * d.gshift);
+      cy = w >> d.gshift;
+      cx = w & (d.grid - 1);
+    } else {
+      const int per = d.grid * d.grid;
+      m = z / per;
+      const int w = z - m * per;
+      cy = w / d.grid;
+      cx = w - cy * d.grid;
+    }
+    return (int64_t)m * d.map_bytes + (int64_t)(cy * d.s + y) * d.atlas_dim + (cx * d.s + x);
   }
-  return (z * d.ny + y) * d.nx + x;
+  return ((int64_t)z * d.ny + y) * d.nx + x;
 }
 
 // Store 8 consecutive level bytes (x .. x+7 on one row): one 8-byte store
@@ -89,7 +98,12 @@ __device__ __forceinline__ void store8(uint8_t* p, uint32_t lo, uint32_t hi) {
 
 inline LevelDst make_dst(const ctp_level_out& lo, int64_t nx, int64_t ny, int64_t z_off_atlas = 0) {
   LevelDst d;
-  d.z_off = lo.layout == CTP_LAYOUT_ATLAS ? z_off_atlas : 0;
+  d.z_off = lo.layout == CTP_LAYOUT_ATLAS ? (int32_t)z_off_atlas : 0;
+  d.gshift = -1;
+  if (lo.grid > 0 && (lo.grid & (lo.grid - 1)) == 0) {
+    d.gshift = 0;
+    while ((1 << d.gshift) < lo.grid) d.gshift++;
+  }
   d.out = lo.out;
   d.layout = lo.layout;
   d.s = lo.s;

@@ -12,20 +12,24 @@
 //   atlases  = encode_slicemaps(level, scheme) packing  slicemap.py:120-142
 //              (+ _pad_to_cube, pipeline.py:226-237, for levels smaller than s)
 //
-// Work decomposition (B200: 148 SMs, 2 resident 256-thread CTAs per SM):
-//   * a TILE is 2^L z-slices x (ky*2^L) rows x (TXu*UXW) columns, <= 1024 UNITS;
-//     CTAs are persistent and walk tiles in memory order.
+// Work decomposition (B200: 148 SMs, persistent CTAs of 256 threads):
+//   * a TILE is 2^L z-slices x (ky*2^L) rows x (TXu*UXW) columns, <= 1024 UNITS,
+//     tiles walked in memory order;
 //   * a UNIT is UXW x-voxels (one 16-byte vector: 16 u8 or 8 u16) on 2 rows x
 //     2 slices (L >= 1) -- exactly the 2x2x2 cells of level 1 along one vector.
-//     Each thread owns 4 units per tile: 16 independent 16-byte loads in flight.
+//     Each thread owns the same 4 unit slots in every tile (coordinates computed
+//     once), loaded as 16-byte vectors, 4 or 8 in flight per thread;
 //   * histogram + LUT in ONE shared-memory atomic per voxel: the counter word
-//     holds lut[v] in bits 0..7 and the count in bits 12..31; atomicAdd(+4096)
+//     holds lut[v] in bits 0..7 and the count in bits 12..31; atom.add(+4096)
 //     returns the old word whose low byte is f = lut[v].  Summing the 8 old
 //     words of a level-1 cell and masking 12 bits gives sum(f) exactly (<= 2040).
-//     u8: per-lane columns [bin][lane] (bank == lane, conflict-free);
-//     u16: one 4096-word table per CTA.
+//     Per voxel the hot loop is PRMT (byte) + LEA (address) + ATOMS + 1/2 IADD3.
+//     u8 tables: per-lane columns [bin][lane] (bank == lane: conflict-free for
+//     any data) or warp-private [warp][bin] (same-address lanes merge: faster on
+//     concentrated histograms); u16: one 4096-word table per CTA;
 //   * level-1 sums go to shared memory; levels 2..L are reduced from there
-//     (u16 / u32 sums) and written, byte per thread, as coalesced row segments.
+//     (u16 / u32 sums) and written as coalesced row segments.
+#include <stdlib.h>
 #include "ctp_common.cuh"
 
 namespace ctp {
@@ -33,23 +37,30 @@ namespace ctp {
 constexpr int kPvThreads = 256;
 constexpr int kMaxUnits = 1024;                 // per tile
 constexpr int kUnitsPerThread = kMaxUnits / kPvThreads;
-constexpr int kBatch = 2;  // units loaded together (8 x 16 B in flight per thread)
 constexpr uint32_t kOne = 1u << 12;             // count increment
 constexpr uint32_t kCountCap = (1u << 20) - 1;  // 20-bit count field
+constexpr int kCellSlots = 4;                   // level-2 cells per thread per tile (<= 1024 / 256)
+
+enum { kLaneCols = 0, kWarpPriv = 1 };
 
 template <typename T> struct Vox;
 template <> struct Vox<uint8_t> {
-  static constexpr int UXW = 16, NBINS = 256, HWORDS = 256 * 32;
+  static constexpr int UXW = 16, NBINS = 256;
 };
 template <> struct Vox<uint16_t> {
-  static constexpr int UXW = 8, NBINS = 4096, HWORDS = 4096;
+  static constexpr int UXW = 8, NBINS = 4096;
+};
+
+template <typename T, int LAYOUT>
+struct Table {
+  static constexpr int WORDS = sizeof(T) == 2 ? 4096 : (LAYOUT == kLaneCols ? 256 * 32 : 256 * (kPvThreads / 32));
 };
 
 struct PvGeom {
   int64_t nx, ny, nz, z_base;
-  int32_t txu;      // units per tile along x
-  int32_t ty;       // rows per tile (multiple of 2^L)
-  int64_t tiles_x, tiles_y, n_tiles;
+  int32_t txu;          // units per tile along x
+  int32_t ty;           // rows per tile (multiple of 2^L)
+  int32_t tiles_x, tiles_y, n_tiles;
   int32_t flush_tiles;  // flush the smem counters every this many tiles
 };
 
@@ -61,41 +72,29 @@ struct PvArgs {
   PvGeom g;
 };
 
-template <typename T>
-__device__ __forceinline__ uint32_t hist_word(uint32_t v, int lane) {
-  if constexpr (sizeof(T) == 1) return (v << 5) | (uint32_t)lane;
-  else return min(v, 4095u);
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
+  return old;
 }
 
-// Process one 32-bit word of voxels: 4 u8 or 2 u16.  Returns old counter words.
-template <typename T>
-__device__ __forceinline__ void atom_word(uint32_t* hs, uint32_t w, int lane, uint32_t* o) {
-  if constexpr (sizeof(T) == 1) {
-#pragma unroll
-    for (int b = 0; b < 4; b++) o[b] = atomicAdd(&hs[hist_word<T>((w >> (8 * b)) & 255u, lane)], kOne);
-  } else {
-    o[0] = atomicAdd(&hs[hist_word<T>(w & 0xFFFFu, lane)], kOne);
-    o[1] = atomicAdd(&hs[hist_word<T>(w >> 16, lane)], kOne);
-  }
-}
-
-template <typename T>
+template <typename T, int LAYOUT>
 __device__ void flush_counts(uint32_t* hs, unsigned long long* hist) {
-  constexpr int NB = Vox<T>::NBINS;
   __syncthreads();
   if constexpr (sizeof(T) == 1) {
     const int bin = threadIdx.x;  // 256 threads == 256 bins
     uint32_t s = 0;
+    constexpr int COPIES = LAYOUT == kLaneCols ? 32 : kPvThreads / 32;
 #pragma unroll 8
-    for (int k = 0; k < 32; k++) {
-      const int idx = bin * 32 + ((k + bin) & 31);
+    for (int k = 0; k < COPIES; k++) {
+      const int idx = LAYOUT == kLaneCols ? bin * 32 + ((k + bin) & 31) : k * 256 + bin;
       const uint32_t wv = hs[idx];
       s += wv >> 12;
       hs[idx] = wv & 0xFFFu;
     }
     if (s && hist) atomicAdd(hist + bin, (unsigned long long)s);
   } else {
-    for (int b = threadIdx.x; b < NB; b += kPvThreads) {
+    for (int b = threadIdx.x; b < 4096; b += kPvThreads) {
       const uint32_t wv = hs[b];
       if ((wv >> 12) && hist) atomicAdd(hist + b, (unsigned long long)(wv >> 12));
       hs[b] = wv & 0xFFFu;
@@ -104,10 +103,32 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist) {
   __syncthreads();
 }
 
-template <typename T, int L>
-__global__ void __launch_bounds__(kPvThreads, 2) preview_kernel(const PvArgs a) {
+// One 16-byte row vector of a unit: UXW atomics; returns the old counter words.
+template <typename T, int LAYOUT>
+__device__ __forceinline__ void row_atomics(const uint4& q, uint32_t lb, uint32_t* o) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  if constexpr (sizeof(T) == 1) {
+    constexpr int SH = LAYOUT == kLaneCols ? 7 : 2;  // bytes per bin row: 32 lanes x 4 B, or 4 B
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        const uint32_t v = __byte_perm(w[k], 0u, 0x4440u | (uint32_t)b);
+        o[4 * k + b] = atom_add_shared(lb + (v << SH), kOne);
+      }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      o[2 * k] = atom_add_shared(lb + (min(w[k] & 0xFFFFu, 4095u) << 2), kOne);
+      o[2 * k + 1] = atom_add_shared(lb + (min(w[k] >> 16, 4095u) << 2), kOne);
+    }
+  }
+}
+
+template <typename T, int L, int MINB, int kBatch, int LAYOUT>
+__global__ void __launch_bounds__(kPvThreads, MINB) preview_kernel(const PvArgs a) {
   constexpr int UXW = Vox<T>::UXW;
-  constexpr int HW = Vox<T>::HWORDS;
+  constexpr int HW = Table<T, LAYOUT>::WORDS;
   constexpr int UZ = (L == 0) ? 1 : 2;
   constexpr int ROWS = UZ * UZ;
   constexpr int TZ = 1 << L;
@@ -118,126 +139,155 @@ __global__ void __launch_bounds__(kPvThreads, 2) preview_kernel(const PvArgs a) 
   uint16_t* s1 = reinterpret_cast<uint16_t*>(smem + HW);        // level-1 sums
   uint32_t* s2 = reinterpret_cast<uint32_t*>(s1 + kMaxUnits * L1PU);  // level-2 sums
   uint32_t* s3 = s2 + kMaxUnits * L1PU / 8;                     // level-3 sums
-  uint32_t* sl[5] = {nullptr, nullptr, s2, s3, nullptr};
 
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const PvGeom& g = a.g;
 
   // counter words: LUT value in the low byte, count 0
   for (int i = threadIdx.x; i < HW; i += kPvThreads) {
-    const int bin = (sizeof(T) == 1) ? (i >> 5) : i;
+    int bin;
+    if constexpr (sizeof(T) == 2) bin = i;
+    else bin = (LAYOUT == kLaneCols) ? (i >> 5) : (i & 255);
     hs[i] = a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255);
   }
+  // this thread's table base in the shared window
+  const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
+  uint32_t lb;
+  if constexpr (sizeof(T) == 2) lb = tbl;
+  else lb = (LAYOUT == kLaneCols) ? tbl + 4u * (uint32_t)lane : tbl + 1024u * (uint32_t)warp;
   __syncthreads();
 
   const int rows_u = g.ty / UZ;               // unit rows along y in a tile
   const int units = (TZ / UZ) * rows_u * g.txu;
   const int xw = g.txu * UXW;                 // tile width in voxels
+  const int64_t sy = g.nx, sz = g.nx * g.ny;
   const T* __restrict__ vol = reinterpret_cast<const T*>(a.vol);
-  int since_flush = 0;
 
-  for (int64_t tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
-    const int64_t tx_i = tile % g.tiles_x;
-    const int64_t rest = tile / g.tiles_x;
-    const int64_t ty_i = rest % g.tiles_y;
-    const int64_t tz_i = rest / g.tiles_y;
-    const int64_t x0 = tx_i * xw, y0 = ty_i * g.ty, z0 = tz_i * TZ;
+  // unit slots of this thread: identical in every tile
+  int uxu[kUnitsPerThread], uyr[kUnitsPerThread], uzr[kUnitsPerThread];
+  int64_t uoff[kUnitsPerThread];
+#pragma unroll
+  for (int i = 0; i < kUnitsPerThread; i++) {
+    const int u = threadIdx.x + kPvThreads * i;
+    uxu[i] = u % g.txu;
+    const int r = u / g.txu;
+    uyr[i] = r % rows_u;
+    uzr[i] = u < units ? r / rows_u : TZ;   // TZ marks "slot unused"
+    uoff[i] = (int64_t)(uzr[i] * UZ) * sz + (int64_t)(uyr[i] * UZ) * sy + uxu[i] * UXW;
+  }
 
-    // ---- load + process in batches of kBatch units (16-byte vectors) ----------
-#pragma unroll 1
-    for (int bt = 0; bt < kUnitsPerThread; bt += kBatch) {
-    uint4 q[kBatch][ROWS];
-    bool ok[kBatch];
+  // level-2..L cell slots of this thread (packed xq | yq << 12 | zq << 24; -1 = none),
+  // kept in shared memory [slot][thread] to spare registers
+  int* cslot = reinterpret_cast<int*>(s3 + kMaxUnits * L1PU / 64 + 4);
+  if constexpr (L >= 2) {
 #pragma unroll
-    for (int i = 0; i < kBatch; i++) {
-      const int u = threadIdx.x + kPvThreads * (bt + i);
-      const int xu = u % g.txu;
-      const int r = u / g.txu;
-      const int yr = r % rows_u;
-      const int zr = r / rows_u;
-      const int64_t x = x0 + (int64_t)xu * UXW, y = y0 + (int64_t)yr * UZ, z = z0 + (int64_t)zr * UZ;
-      ok[i] = (u < units) && (x < g.nx) && (y < g.ny);
-      if (ok[i]) {
-#pragma unroll
-        for (int r2 = 0; r2 < ROWS; r2++) {
-          const int dz = r2 / UZ, dy = r2 % UZ;
-          q[i][r2] = __ldcs(reinterpret_cast<const uint4*>(vol + ((z + dz) * g.ny + (y + dy)) * g.nx + x));
+    for (int sl = 0; sl < kCellSlots + 2; sl++) {
+      const int l = sl < kCellSlots ? 2 : sl - kCellSlots + 3;
+      const int k = sl < kCellSlots ? sl : 0;
+      int code = -1;
+      if (l <= L) {
+        const int nzc = TZ >> l, nyc = g.ty >> l, nxc = xw >> l;
+        const int c = threadIdx.x + kPvThreads * k;
+        if (c < nzc * nyc * nxc) {
+          const int xq = c % nxc, yq = (c / nxc) % nyc, zq = c / (nxc * nyc);
+          code = xq | (yq << 12) | (zq << 24);
         }
       }
+      cslot[sl * kPvThreads + threadIdx.x] = code;
     }
+  }
 
-    // ---- histogram + LUT + level 0/1 -----------------------------------------
-#pragma unroll
-    for (int i = 0; i < kBatch; i++) {
-      if (!ok[i]) continue;
-      const int u = threadIdx.x + kPvThreads * (bt + i);
-      const int xu = u % g.txu;
-      const int r = u / g.txu;
-      const int yr = r % rows_u;
-      const int zr = r / rows_u;
-      const int64_t x = x0 + (int64_t)xu * UXW, y = y0 + (int64_t)yr * UZ, z = z0 + (int64_t)zr * UZ;
+  int since_flush = 0;
+  for (int tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
+    const int tx_i = tile % g.tiles_x;
+    const int rest = tile / g.tiles_x;
+    const int ty_i = rest % g.tiles_y;
+    const int tz_i = rest / g.tiles_y;
+    const int x0 = tx_i * xw, y0 = ty_i * g.ty, z0 = tz_i * TZ;
+    const T* tile_base = vol + (int64_t)z0 * sz + (int64_t)y0 * sy + x0;
 
-      // per row: UXW atomics (hist + LUT), optional level-0 store, and the
-      // running level-1 pair sums (low 12 bits of the summed old words)
-      uint32_t acc[L1PU];
 #pragma unroll
-      for (int j = 0; j < L1PU; j++) acc[j] = 0;
+    for (int bt = 0; bt < kUnitsPerThread; bt += kBatch) {
+      uint4 q[kBatch][ROWS];
+      bool ok[kBatch];
 #pragma unroll
-      for (int r2 = 0; r2 < ROWS; r2++) {
-        uint32_t o[UXW];
-        const uint32_t w[4] = {q[i][r2].x, q[i][r2].y, q[i][r2].z, q[i][r2].w};
+      for (int i = 0; i < kBatch; i++) {
+        const int s = bt + i;
+        ok[i] = (uzr[s] < TZ / UZ) && (x0 + uxu[s] * UXW < g.nx) && (y0 + uyr[s] * UZ < g.ny);
+        if (ok[i]) {
+          const T* p = tile_base + uoff[s];
 #pragma unroll
-        for (int k = 0; k < 4; k++) atom_word<T>(hs, w[k], lane, &o[k * (UXW / 4)]);
-        if (a.lv[0].out) {  // level 0: the filtered voxels themselves
-          const int dz = r2 / UZ, dy = r2 % UZ;
-          uint8_t* dst = a.lv[0].out + level_offset(a.lv[0], z + dz, y + dy, x);
-          uint32_t pk[UXW / 4];
+          for (int r2 = 0; r2 < ROWS; r2++)
+            q[i][r2] = __ldcs(reinterpret_cast<const uint4*>(p + (r2 / UZ) * sz + (r2 % UZ) * sy));
+        }
+      }
+
 #pragma unroll
-          for (int k = 0; k < UXW / 4; k++)
-            pk[k] = __byte_perm(__byte_perm(o[4 * k], o[4 * k + 1], 0x0040),
-                                __byte_perm(o[4 * k + 2], o[4 * k + 3], 0x0040), 0x5410);
-          if constexpr (UXW == 16) {
-            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            else { store8(dst, pk[0], pk[1]); store8(dst + 8, pk[2], pk[3]); }
-          } else {
-            store8(dst, pk[0], pk[1]);
+      for (int i = 0; i < kBatch; i++) {
+        if (!ok[i]) continue;
+        const int s = bt + i;
+        const int xu = uxu[s], yr = uyr[s], zr = uzr[s];
+        const int x = x0 + xu * UXW, y = y0 + yr * UZ, z = z0 + zr * UZ;
+        uint32_t acc[L1PU];
+#pragma unroll
+        for (int j = 0; j < L1PU; j++) acc[j] = 0;
+#pragma unroll
+        for (int r2 = 0; r2 < ROWS; r2++) {
+          uint32_t o[UXW];
+          row_atomics<T, LAYOUT>(q[i][r2], lb, o);
+          if (a.lv[0].out) {  // level 0: the filtered voxels themselves
+            uint8_t* dst = a.lv[0].out + level_offset(a.lv[0], z + r2 / UZ, y + r2 % UZ, x);
+            uint32_t pk[UXW / 4];
+#pragma unroll
+            for (int k = 0; k < UXW / 4; k++)
+              pk[k] = __byte_perm(__byte_perm(o[4 * k], o[4 * k + 1], 0x0040),
+                                  __byte_perm(o[4 * k + 2], o[4 * k + 3], 0x0040), 0x5410);
+            if constexpr (UXW == 16) {
+              if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+                *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              else {
+                store8(dst, pk[0], pk[1]);
+                store8(dst + 8, pk[2], pk[3]);
+              }
+            } else {
+              store8(dst, pk[0], pk[1]);
+            }
+          }
+          if constexpr (L >= 1) {
+#pragma unroll
+            for (int j = 0; j < L1PU; j++) acc[j] += o[2 * j] + o[2 * j + 1];
           }
         }
         if constexpr (L >= 1) {
+          uint32_t sum[L1PU];
 #pragma unroll
-          for (int j = 0; j < L1PU; j++) acc[j] += o[2 * j] + o[2 * j + 1];
+          for (int j = 0; j < L1PU; j++) sum[j] = acc[j] & 0xFFFu;  // sum of f over the 2x2x2 cell (<= 2040)
+          if (a.lv[1].out) {
+            uint32_t pk[L1PU / 4];
+#pragma unroll
+            for (int k = 0; k < L1PU / 4; k++)
+              pk[k] = ((sum[4 * k] + 4) >> 3) | (((sum[4 * k + 1] + 4) >> 3) << 8) |
+                      (((sum[4 * k + 2] + 4) >> 3) << 16) | (((sum[4 * k + 3] + 4) >> 3) << 24);
+            uint8_t* dst = a.lv[1].out + level_offset(a.lv[1], z >> 1, y >> 1, x >> 1);
+            if constexpr (L1PU == 8) {
+              store8(dst, pk[0], pk[1]);
+            } else {
+              if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = pk[0];
+              else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(pk[0] >> (8 * b));
+            }
+          }
+          if constexpr (L >= 2) {
+            // s1 layout [zr][yr][x1], x1 = xu*L1PU + j
+            uint16_t* d = s1 + ((zr * rows_u + yr) * g.txu + xu) * L1PU;
+            if constexpr (L1PU == 8)
+              *reinterpret_cast<uint4*>(d) = make_uint4(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16),
+                                                        sum[4] | (sum[5] << 16), sum[6] | (sum[7] << 16));
+            else
+              *reinterpret_cast<uint2*>(d) = make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
+          }
         }
       }
-      if constexpr (L >= 1) {
-        uint32_t sum[L1PU];
-#pragma unroll
-        for (int j = 0; j < L1PU; j++) sum[j] = acc[j] & 0xFFFu;  // sum of f over the 2x2x2 cell (<= 2040)
-        if (a.lv[1].out) {
-          uint32_t pk[L1PU / 4];
-#pragma unroll
-          for (int k = 0; k < L1PU / 4; k++) {
-            pk[k] = ((sum[4 * k] + 4) >> 3) | (((sum[4 * k + 1] + 4) >> 3) << 8) |
-                    (((sum[4 * k + 2] + 4) >> 3) << 16) | (((sum[4 * k + 3] + 4) >> 3) << 24);
-          }
-          uint8_t* dst = a.lv[1].out + level_offset(a.lv[1], z >> 1, y >> 1, x >> 1);
-          if constexpr (L1PU == 8) store8(dst, pk[0], pk[1]);
-          else {
-            if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = pk[0];
-            else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(pk[0] >> (8 * b));
-          }
-        }
-        if constexpr (L >= 2) {
-          // s1 layout [zr][yr][x1], x1 = xu*L1PU + j
-          uint16_t* d = s1 + ((size_t)(zr * rows_u + yr) * g.txu + xu) * L1PU;
-          if constexpr (L1PU == 8)
-            *reinterpret_cast<uint4*>(d) = make_uint4(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16),
-                                                      sum[4] | (sum[5] << 16), sum[6] | (sum[7] << 16));
-          else
-            *reinterpret_cast<uint2*>(d) = make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
-        }
-      }
-    }
-
     }  // batch loop
 
     // ---- levels 2..L from shared memory ----------------------------------------
@@ -245,17 +295,19 @@ __global__ void __launch_bounds__(kPvThreads, 2) preview_kernel(const PvArgs a) 
       __syncthreads();
 #pragma unroll
       for (int l = 2; l <= L; l++) {
-        const int cz = TZ >> (l - 1), cy = g.ty >> (l - 1), cx = xw >> (l - 1);  // child dims
-        const int nzc = cz >> 1, nyc = cy >> 1, nxc = cx >> 1;
-        const int cells = nzc * nyc * nxc;
-        const int64_t lnx = g.nx >> l, lny = g.ny >> l;
+        const int cy = g.ty >> (l - 1), cx = xw >> (l - 1);  // child dims (y, x)
+        const int lnx = (int)(g.nx >> l), lny = (int)(g.ny >> l);
         const int shift = 3 * l;
-        for (int c = threadIdx.x; c < cells; c += kPvThreads) {
-          const int xq = c % nxc;
-          const int rr = c / nxc;
-          const int yq = rr % nyc;
-          const int zq = rr / nyc;
-          const int64_t gx = (x0 >> l) + xq, gy = (y0 >> l) + yq;
+        uint32_t* dsts = (l == 2) ? s2 : s3;
+        const uint32_t* srcs = (l == 3) ? s2 : s3;
+        const bool want = a.lv[l].out != nullptr;
+#pragma unroll
+        for (int k = 0; k < kCellSlots; k++) {
+          if (l > 2 && k > 0) break;
+          const int code = cslot[(l == 2 ? k : kCellSlots + l - 3) * kPvThreads + threadIdx.x];
+          if (code < 0) continue;
+          const int xq = code & 0xFFF, yq = (code >> 12) & 0xFFF, zq = code >> 24;
+          const int gx = (x0 >> l) + xq, gy = (y0 >> l) + yq;
           if (gx >= lnx || gy >= lny) continue;
           uint32_t sum = 0;
 #pragma unroll
@@ -267,15 +319,13 @@ __global__ void __launch_bounds__(kPvThreads, 2) preview_kernel(const PvArgs a) 
                 const uint32_t pair = *reinterpret_cast<const uint32_t*>(s1 + base);
                 sum += (pair & 0xFFFFu) + (pair >> 16);
               } else {
-                const uint32_t* src = sl[l - 1];
-                sum += src[base] + src[base + 1];
+                sum += srcs[base] + srcs[base + 1];
               }
             }
-          if (l < L) sl[l][c] = sum;
-          if (a.lv[l].out) {
-            const int64_t gz = (z0 >> l) + zq;
-            a.lv[l].out[level_offset(a.lv[l], gz, gy, gx)] = (uint8_t)((sum + (1u << (shift - 1))) >> shift);
-          }
+          if (l < L) dsts[threadIdx.x + kPvThreads * k] = sum;
+          if (want)
+            a.lv[l].out[level_offset(a.lv[l], (z0 >> l) + zq, gy, gx)] =
+                (uint8_t)((sum + (1u << (shift - 1))) >> shift);
         }
         __syncthreads();
       }
@@ -283,29 +333,67 @@ __global__ void __launch_bounds__(kPvThreads, 2) preview_kernel(const PvArgs a) 
 
     if (++since_flush == g.flush_tiles) {
       since_flush = 0;
-      flush_counts<T>(hs, a.hist);
+      flush_counts<T, LAYOUT>(hs, a.hist);
     }
   }
-  flush_counts<T>(hs, a.hist);
+  flush_counts<T, LAYOUT>(hs, a.hist);
 }
 
-template <typename T>
+template <typename T, int LAYOUT>
 static size_t smem_bytes(int L) {
-  size_t b = (size_t)Vox<T>::HWORDS * 4;
+  size_t b = (size_t)Table<T, LAYOUT>::WORDS * 4;
   if (L >= 2) {
     const size_t l1 = (size_t)kMaxUnits * (Vox<T>::UXW / 2);
-    b += l1 * 2 + (l1 / 8) * 4 + (l1 / 64) * 4 + 16;
+    b += l1 * 2 + (l1 / 8) * 4 + (l1 / 64) * 4 + 16 + (kCellSlots + 2) * kPvThreads * 4;
   }
   return b;
 }
 
-template <typename T, int L>
-static int launch_l(const PvArgs& a, int grid, cudaStream_t st) {
-  const size_t sm = smem_bytes<T>(L);
-  CTP_CUDA_CALL(cudaFuncSetAttribute(preview_kernel<T, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  preview_kernel<T, L><<<grid, kPvThreads, sm, st>>>(a);
+template <typename T, int L, int MINB, int BATCH, int LAYOUT>
+static int launch_v(PvArgs a, cudaStream_t st) {
+  const size_t sm = smem_bytes<T, LAYOUT>(L);
+  auto kern = preview_kernel<T, L, MINB, BATCH, LAYOUT>;
+  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  // a counter word gains at most this many counts per tile
+  constexpr int UZ = L == 0 ? 1 : 2;
+  const int64_t vox_per_unit = (int64_t)Vox<T>::UXW * UZ * UZ;
+  int64_t per_tile;
+  if (sizeof(T) == 2) per_tile = (int64_t)kMaxUnits * vox_per_unit;                // whole CTA
+  else if (LAYOUT == kLaneCols) per_tile = 8LL * kUnitsPerThread * vox_per_unit;    // one lane of 8 warps
+  else per_tile = 32LL * kUnitsPerThread * vox_per_unit;                            // one warp
+  a.g.flush_tiles = (int)(kCountCap / per_tile);
+  if (a.g.flush_tiles < 1) a.g.flush_tiles = 1;
+  int grid = num_sms() * MINB;
+  if (a.g.n_tiles < grid) grid = a.g.n_tiles;
+  kern<<<grid, kPvThreads, sm, st>>>(a);
   CTP_CUDA_CHECK_LAUNCH("preview_kernel");
   return CTP_OK;
+}
+
+// Launch-shape variants, selectable with CTP_PREVIEW_VARIANT for tuning
+// (tools/prof_preview.py); the default was the fastest measured on B200.
+static int preview_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTP_PREVIEW_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <typename T, int L>
+static int launch_l(const PvArgs& a, cudaStream_t st) {
+  if constexpr (sizeof(T) == 1) {
+    switch (preview_variant()) {
+      case 1: return launch_v<T, L, 3, 1, kLaneCols>(a, st);
+      case 2: return launch_v<T, L, 2, 2, kWarpPriv>(a, st);
+      case 3: return launch_v<T, L, 3, 1, kWarpPriv>(a, st);
+      case 4: return launch_v<T, L, 4, 1, kLaneCols>(a, st);
+      default: return launch_v<T, L, 2, 2, kLaneCols>(a, st);
+    }
+  } else {
+    return launch_v<T, L, 2, 2, kLaneCols>(a, st);
+  }
 }
 
 template <typename T>
@@ -314,6 +402,7 @@ static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_
   constexpr int UXW = Vox<T>::UXW;
   CTP_REQUIRE(vol != nullptr && levels != nullptr, CTP_E_INVALID, "preview: null pointer");
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1, CTP_E_INVALID, "preview: degenerate shape");
+  CTP_REQUIRE(nx < (1LL << 30) && ny < (1LL << 30) && nz < (1LL << 30), CTP_E_INVALID, "preview: shape too large");
   CTP_REQUIRE(nlev >= 0 && nlev <= 4, CTP_E_INVALID, "preview: nlev %d outside [0, 4]", nlev);
   CTP_REQUIRE((reinterpret_cast<uintptr_t>(vol) & 15) == 0, CTP_E_ALIGN, "preview: volume not 16-byte aligned");
   CTP_REQUIRE(nx % UXW == 0, CTP_E_ALIGN, "preview: nx=%lld not a multiple of %d", (long long)nx, UXW);
@@ -355,26 +444,22 @@ static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_
     g.txu = (int)(kMaxUnits / urows_per_block);
     g.ty = (int)blk;
   }
-  g.tiles_x = (xu_total + g.txu - 1) / g.txu;
-  g.tiles_y = (ny + g.ty - 1) / g.ty;
-  g.n_tiles = g.tiles_x * g.tiles_y * (nz / tz);
-  // a counter word gains at most (units per thread) * (voxels per unit) per warp per tile,
-  // from 8 warps (u8 lane columns) or from every thread (u16 shared table)
-  const int64_t vox_per_unit = (int64_t)UXW * uz * uz;
-  const int64_t per_tile = (sizeof(T) == 1) ? 8LL * kUnitsPerThread * vox_per_unit
-                                            : (int64_t)kMaxUnits * vox_per_unit;
-  g.flush_tiles = (int)(kCountCap / per_tile);
-  if (g.flush_tiles < 1) g.flush_tiles = 1;
+  const int64_t tiles_x = (xu_total + g.txu - 1) / g.txu;
+  const int64_t tiles_y = (ny + g.ty - 1) / g.ty;
+  const int64_t n_tiles = tiles_x * tiles_y * (nz / tz);
+  CTP_REQUIRE(n_tiles < (1LL << 31), CTP_E_INVALID, "preview: too many tiles");
+  g.tiles_x = (int)tiles_x;
+  g.tiles_y = (int)tiles_y;
+  g.n_tiles = (int)n_tiles;
+  g.flush_tiles = 1;
 
-  int grid = num_sms() * 2;
-  if (g.n_tiles < grid) grid = (int)g.n_tiles;
   cudaStream_t st = as_stream(stream);
   switch (nlev) {
-    case 0: return launch_l<T, 0>(a, grid, st);
-    case 1: return launch_l<T, 1>(a, grid, st);
-    case 2: return launch_l<T, 2>(a, grid, st);
-    case 3: return launch_l<T, 3>(a, grid, st);
-    default: return launch_l<T, 4>(a, grid, st);
+    case 0: return launch_l<T, 0>(a, st);
+    case 1: return launch_l<T, 1>(a, st);
+    case 2: return launch_l<T, 2>(a, st);
+    case 3: return launch_l<T, 3>(a, st);
+    default: return launch_l<T, 4>(a, st);
   }
 }
 
