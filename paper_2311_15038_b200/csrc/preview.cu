@@ -12,89 +12,114 @@
 //   atlases  = encode_slicemaps(level, scheme) packing  slicemap.py:120-142
 //              (+ _pad_to_cube, pipeline.py:226-237, for levels smaller than s)
 //
-// Work decomposition (B200: 148 SMs, persistent CTAs of 256 threads):
-//   * a TILE is 2^L z-slices x (ky*2^L) rows x (TXu*UXW) columns, <= 1024 UNITS,
-//     tiles walked in memory order;
+// B200 mapping (148 SMs, one persistent CTA per SM):
+//   * a TILE is 2^L z-slices x (ky*2^L) rows x (TXu*UXW) columns, <= MAXU units.
+//     Tiles stream from HBM into a ring of NST shared-memory stages with TMA
+//     (cp.async.bulk.tensor.3d, boxes of <= 256 x ty x 2^L elements, completion
+//     on an mbarrier): while the CTA reduces tile k, tiles k+1..k+NST-1 are in
+//     flight, and no register is spent on in-flight data.
 //   * a UNIT is UXW x-voxels (one 16-byte vector: 16 u8 or 8 u16) on 2 rows x
-//     2 slices (L >= 1) -- exactly the 2x2x2 cells of level 1 along one vector.
-//     Each thread owns the same 4 unit slots in every tile (coordinates computed
-//     once), loaded as 16-byte vectors, 4 or 8 in flight per thread;
+//     2 slices (L >= 1) -- exactly the 2x2x2 cells of level 1 along one vector;
+//     every thread owns the same unit slots in every tile (offsets computed once).
 //   * histogram + LUT in ONE shared-memory atomic per voxel: the counter word
 //     holds lut[v] in bits 0..7 and the count in bits 12..31; atom.add(+4096)
 //     returns the old word whose low byte is f = lut[v].  Summing the 8 old
 //     words of a level-1 cell and masking 12 bits gives sum(f) exactly (<= 2040).
-//     Per voxel the hot loop is PRMT (byte) + LEA (address) + ATOMS + 1/2 IADD3.
-//     u8 tables: per-lane columns [bin][lane] (bank == lane: conflict-free for
-//     any data) or warp-private [warp][bin] (same-address lanes merge: faster on
-//     concentrated histograms); u16: one 4096-word table per CTA;
+//     Per voxel the hot loop is PRMT (byte) + IMAD (address) + ATOMS + 1/2 add.
+//     u8: per-lane columns [bin][lane] -- bank == lane, so a warp-wide ATOMS is
+//     conflict-free for any data (tools/microbench/hist_bench.cu); u16: one
+//     4096-word table per CTA.
 //   * level-1 sums go to shared memory; levels 2..L are reduced from there
 //     (u16 / u32 sums) and written as coalesced row segments.
 #include <stdlib.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 #include "ctp_common.cuh"
 
 namespace ctp {
 
-constexpr int kPvThreads = 256;
-constexpr int kMaxUnits = 1024;                 // per tile
-constexpr int kUnitsPerThread = kMaxUnits / kPvThreads;
 constexpr uint32_t kOne = 1u << 12;             // count increment
 constexpr uint32_t kCountCap = (1u << 20) - 1;  // 20-bit count field
-constexpr int kCellSlots = 4;                   // level-2 cells per thread per tile (<= 1024 / 256)
-
-enum { kLaneCols = 0, kWarpPriv = 1 };
+constexpr int kBoxX = 256;                      // TMA box limit per dimension (elements)
 
 template <typename T> struct Vox;
 template <> struct Vox<uint8_t> {
-  static constexpr int UXW = 16, NBINS = 256;
+  static constexpr int UXW = 16, NBINS = 256, HWORDS = 256 * 32;
 };
 template <> struct Vox<uint16_t> {
-  static constexpr int UXW = 8, NBINS = 4096;
-};
-
-template <typename T, int LAYOUT>
-struct Table {
-  static constexpr int WORDS = sizeof(T) == 2 ? 4096 : (LAYOUT == kLaneCols ? 256 * 32 : 256 * (kPvThreads / 32));
+  static constexpr int UXW = 8, NBINS = 4096, HWORDS = 4096;
 };
 
 struct PvGeom {
-  int64_t nx, ny, nz, z_base;
+  int32_t nx, ny, nz;
   int32_t txu;          // units per tile along x
   int32_t ty;           // rows per tile (multiple of 2^L)
   int32_t tiles_x, tiles_y, n_tiles;
   int32_t flush_tiles;  // flush the smem counters every this many tiles
+  int32_t box_x;        // TMA box width (elements); a tile is nboxes boxes side by side
+  int32_t nboxes;
+  uint32_t box_bytes;   // box_x * ty * 2^L * sizeof(T)
 };
 
 struct PvArgs {
-  const void* vol;
   const uint8_t* lut;
   unsigned long long* hist;
   LevelDst lv[CTP_MAX_LEVELS];
   PvGeom g;
 };
 
+// ---- PTX helpers -------------------------------------------------------------
 __device__ __forceinline__ uint32_t atom_add_shared(uint32_t addr, uint32_t v) {
   uint32_t old;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v));
   return old;
 }
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
 
-template <typename T, int LAYOUT>
-__device__ void flush_counts(uint32_t* hs, unsigned long long* hist) {
+template <typename T>
+__device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads) {
   __syncthreads();
   if constexpr (sizeof(T) == 1) {
-    const int bin = threadIdx.x;  // 256 threads == 256 bins
-    uint32_t s = 0;
-    constexpr int COPIES = LAYOUT == kLaneCols ? 32 : kPvThreads / 32;
+    for (int bin = threadIdx.x; bin < 256; bin += threads) {
+      uint32_t s = 0;
 #pragma unroll 8
-    for (int k = 0; k < COPIES; k++) {
-      const int idx = LAYOUT == kLaneCols ? bin * 32 + ((k + bin) & 31) : k * 256 + bin;
-      const uint32_t wv = hs[idx];
-      s += wv >> 12;
-      hs[idx] = wv & 0xFFFu;
+      for (int k = 0; k < 32; k++) {
+        const int idx = bin * 32 + ((k + bin) & 31);  // rotated: conflict-free
+        const uint32_t wv = hs[idx];
+        s += wv >> 12;
+        hs[idx] = wv & 0xFFFu;
+      }
+      if (s && hist) atomicAdd(hist + bin, (unsigned long long)s);
     }
-    if (s && hist) atomicAdd(hist + bin, (unsigned long long)s);
   } else {
-    for (int b = threadIdx.x; b < 4096; b += kPvThreads) {
+    for (int b = threadIdx.x; b < 4096; b += threads) {
       const uint32_t wv = hs[b];
       if ((wv >> 12) && hist) atomicAdd(hist + b, (unsigned long long)(wv >> 12));
       hs[b] = wv & 0xFFFu;
@@ -104,17 +129,16 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist) {
 }
 
 // One 16-byte row vector of a unit: UXW atomics; returns the old counter words.
-template <typename T, int LAYOUT>
+template <typename T>
 __device__ __forceinline__ void row_atomics(const uint4& q, uint32_t lb, uint32_t* o) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
   if constexpr (sizeof(T) == 1) {
-    constexpr int SH = LAYOUT == kLaneCols ? 7 : 2;  // bytes per bin row: 32 lanes x 4 B, or 4 B
 #pragma unroll
     for (int k = 0; k < 4; k++)
 #pragma unroll
       for (int b = 0; b < 4; b++) {
         const uint32_t v = __byte_perm(w[k], 0u, 0x4440u | (uint32_t)b);
-        o[4 * k + b] = atom_add_shared(lb + (v << SH), kOne);
+        o[4 * k + b] = atom_add_shared(lb + (v << 7), kOne);  // [bin][lane] words: bin row = 128 B
       }
   } else {
 #pragma unroll
@@ -125,124 +149,174 @@ __device__ __forceinline__ void row_atomics(const uint4& q, uint32_t lb, uint32_
   }
 }
 
-template <typename T, int L, int MINB, int kBatch, int LAYOUT>
-__global__ void __launch_bounds__(kPvThreads, MINB) preview_kernel(const PvArgs a) {
-  constexpr int UXW = Vox<T>::UXW;
-  constexpr int HW = Table<T, LAYOUT>::WORDS;
-  constexpr int UZ = (L == 0) ? 1 : 2;
-  constexpr int ROWS = UZ * UZ;
-  constexpr int TZ = 1 << L;
-  constexpr int L1PU = UXW / 2;  // level-1 sums per unit
+template <typename T, int L, int MAXU>
+struct PvLayout {
+  static constexpr int UXW = Vox<T>::UXW;
+  static constexpr int UZ = (L == 0) ? 1 : 2;
+  static constexpr int ROWS = UZ * UZ;
+  static constexpr int L1PU = UXW / 2;
+  static constexpr int STAGE_BYTES = MAXU * ROWS * 16;
+  static constexpr int HIST_BYTES = Vox<T>::HWORDS * 4;
+  static constexpr int S1_BYTES = L >= 2 ? MAXU * L1PU * 2 : 0;
+};
 
-  extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* hs = smem;                                          // HW counter words
-  uint16_t* s1 = reinterpret_cast<uint16_t*>(smem + HW);        // level-1 sums
-  uint32_t* s2 = reinterpret_cast<uint32_t*>(s1 + kMaxUnits * L1PU);  // level-2 sums
-  uint32_t* s3 = s2 + kMaxUnits * L1PU / 8;                     // level-3 sums
+// (sum + 4) >> 3 of two packed 12-bit level-1 sums, as two bytes in 16-bit lanes
+__device__ __forceinline__ uint32_t round_l1_pair(uint32_t p) { return ((p + 0x00040004u) >> 3) & 0x00FF00FFu; }
+
+template <typename T, int L, int THREADS, int NST, int MAXU>
+__global__ void __launch_bounds__(THREADS, 1)
+    preview_kernel(const __grid_constant__ CUtensorMap tmap, const PvArgs a) {
+  using LY = PvLayout<T, L, MAXU>;
+  constexpr int UXW = LY::UXW, UZ = LY::UZ, ROWS = LY::ROWS, L1PU = LY::L1PU;
+  constexpr int TZ = 1 << L;
+  constexpr int UPT = MAXU / THREADS;  // unit slots per thread
+  constexpr int HW = Vox<T>::HWORDS;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint32_t* hs = reinterpret_cast<uint32_t*>(smem + NST * LY::STAGE_BYTES);
+  uint16_t* s1 = reinterpret_cast<uint16_t*>(smem + NST * LY::STAGE_BYTES + LY::HIST_BYTES);
+  // level-1 sums are double-buffered so tile k+1's unit phase may overwrite
+  // nothing that tile k's level phase still reads (one barrier per tile)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s1) + 2 * LY::S1_BYTES);
 
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const PvGeom& g = a.g;
-
-  // counter words: LUT value in the low byte, count 0
-  for (int i = threadIdx.x; i < HW; i += kPvThreads) {
-    int bin;
-    if constexpr (sizeof(T) == 2) bin = i;
-    else bin = (LAYOUT == kLaneCols) ? (i >> 5) : (i & 255);
-    hs[i] = a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255);
-  }
-  // this thread's table base in the shared window
-  const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
-  uint32_t lb;
-  if constexpr (sizeof(T) == 2) lb = tbl;
-  else lb = (LAYOUT == kLaneCols) ? tbl + 4u * (uint32_t)lane : tbl + 1024u * (uint32_t)warp;
-  __syncthreads();
-
-  const int rows_u = g.ty / UZ;               // unit rows along y in a tile
+  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(stages);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(bars);
+  const uint32_t s1a = (uint32_t)__cvta_generic_to_shared(s1);
+  const int xw = g.txu * UXW;  // tile width (elements)
+  const int rows_u = g.ty / UZ;
   const int units = (TZ / UZ) * rows_u * g.txu;
-  const int xw = g.txu * UXW;                 // tile width in voxels
-  const int64_t sy = g.nx, sz = g.nx * g.ny;
-  const T* __restrict__ vol = reinterpret_cast<const T*>(a.vol);
+  const int s1_row = g.txu * L1PU;  // level-1 sums per (z1, y1) row of the tile
 
-  // unit slots of this thread: identical in every tile
-  int uxu[kUnitsPerThread], uyr[kUnitsPerThread], uzr[kUnitsPerThread];
-  int64_t uoff[kUnitsPerThread];
-#pragma unroll
-  for (int i = 0; i < kUnitsPerThread; i++) {
-    const int u = threadIdx.x + kPvThreads * i;
-    uxu[i] = u % g.txu;
-    const int r = u / g.txu;
-    uyr[i] = r % rows_u;
-    uzr[i] = u < units ? r / rows_u : TZ;   // TZ marks "slot unused"
-    uoff[i] = (int64_t)(uzr[i] * UZ) * sz + (int64_t)(uyr[i] * UZ) * sy + uxu[i] * UXW;
-  }
+  // this CTA's contiguous range of tiles (coordinates advance incrementally)
+  const int per = g.n_tiles / gridDim.x, extra = g.n_tiles % gridDim.x;
+  const int t_begin = blockIdx.x * per + min((int)blockIdx.x, extra);
+  const int t_end = t_begin + per + ((int)blockIdx.x < extra ? 1 : 0);
 
-  // level-2..L cell slots of this thread (packed xq | yq << 12 | zq << 24; -1 = none),
-  // kept in shared memory [slot][thread] to spare registers
-  int* cslot = reinterpret_cast<int*>(s3 + kMaxUnits * L1PU / 64 + 4);
-  if constexpr (L >= 2) {
-#pragma unroll
-    for (int sl = 0; sl < kCellSlots + 2; sl++) {
-      const int l = sl < kCellSlots ? 2 : sl - kCellSlots + 3;
-      const int k = sl < kCellSlots ? sl : 0;
-      int code = -1;
-      if (l <= L) {
-        const int nzc = TZ >> l, nyc = g.ty >> l, nxc = xw >> l;
-        const int c = threadIdx.x + kPvThreads * k;
-        if (c < nzc * nyc * nxc) {
-          const int xq = c % nxc, yq = (c / nxc) % nyc, zq = c / (nxc * nyc);
-          code = xq | (yq << 12) | (zq << 24);
-        }
-      }
-      cslot[sl * kPvThreads + threadIdx.x] = code;
-    }
-  }
-
-  int since_flush = 0;
-  for (int tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
+  auto issue = [&](int tile, int stage) {
     const int tx_i = tile % g.tiles_x;
     const int rest = tile / g.tiles_x;
     const int ty_i = rest % g.tiles_y;
     const int tz_i = rest / g.tiles_y;
-    const int x0 = tx_i * xw, y0 = ty_i * g.ty, z0 = tz_i * TZ;
-    const T* tile_base = vol + (int64_t)z0 * sz + (int64_t)y0 * sy + x0;
+    const uint32_t bar = bar0 + 8u * stage;
+    mbar_expect_tx(bar, g.box_bytes * (uint32_t)g.nboxes);
+    for (int b = 0; b < g.nboxes; b++)
+      tma_load_3d(stage0 + (uint32_t)stage * LY::STAGE_BYTES + (uint32_t)b * g.box_bytes, &tmap,
+                  tx_i * xw + b * g.box_x, ty_i * g.ty, tz_i * TZ, bar);
+  };
 
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    for (int s = 0; s < NST; s++) mbar_init(bar0 + 8u * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NST; s++)
+      if (t_begin + s < t_end) issue(t_begin + s, s);
+
+  // counter words: LUT value in the low byte, count 0
+  for (int i = threadIdx.x; i < HW; i += THREADS) {
+    const int bin = (sizeof(T) == 2) ? i : (i >> 5);
+    hs[i] = a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255);
+  }
+  const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
+  const uint32_t lb = (sizeof(T) == 2) ? tbl : tbl + 4u * (uint32_t)lane;
+
+  // unit slots of this thread (same in every tile): coordinates + stage offset
+  int uxu[UPT], uyr[UPT], uzr[UPT];
+  uint32_t uso[UPT];
 #pragma unroll
-    for (int bt = 0; bt < kUnitsPerThread; bt += kBatch) {
-      uint4 q[kBatch][ROWS];
-      bool ok[kBatch];
-#pragma unroll
-      for (int i = 0; i < kBatch; i++) {
-        const int s = bt + i;
-        ok[i] = (uzr[s] < TZ / UZ) && (x0 + uxu[s] * UXW < g.nx) && (y0 + uyr[s] * UZ < g.ny);
-        if (ok[i]) {
-          const T* p = tile_base + uoff[s];
-#pragma unroll
-          for (int r2 = 0; r2 < ROWS; r2++)
-            q[i][r2] = __ldcs(reinterpret_cast<const uint4*>(p + (r2 / UZ) * sz + (r2 % UZ) * sy));
-        }
+  for (int i = 0; i < UPT; i++) {
+    const int u = threadIdx.x + THREADS * i;
+    uxu[i] = u % g.txu;
+    const int r = u / g.txu;
+    uyr[i] = r % rows_u;
+    uzr[i] = u < units ? r / rows_u : TZ;  // TZ marks "slot unused"
+    const int x = uxu[i] * UXW;
+    const int b = x / g.box_x, xi = x - b * g.box_x;
+    uso[i] = (uint32_t)b * g.box_bytes + (uint32_t)(((uzr[i] * UZ) * g.ty + uyr[i] * UZ) * g.box_x + xi) * sizeof(T);
+  }
+  const uint32_t row_dy = (uint32_t)g.box_x * sizeof(T);
+  const uint32_t row_dz = (uint32_t)g.box_x * g.ty * sizeof(T);
+
+  // Level >= 3 reduction slot (tile-invariant): a group of 4 lanes owns one
+  // level-3 cell; lane q = (dz, dy) reduces the two x-adjacent level-2 children
+  // (2z3+dz, 2y3+dy, 2x3 + {0,1}); level 3 = shfl over the 4 lanes; for L = 4
+  // the 8 level-3 children of a level-4 cell are 8 consecutive groups (a warp).
+  int c_x2 = -1, c_y2 = 0, c_z2 = 0;
+  uint32_t c_s1 = 0;
+  if constexpr (L >= 3) {
+    const int nx3 = xw >> 3, ny3 = g.ty >> 3;
+    const int cells3 = (TZ >> 3) * ny3 * nx3;
+    const int grp = threadIdx.x >> 2, q = threadIdx.x & 3;
+    if (grp < cells3) {
+      int x3, y3, z3;
+      if constexpr (L == 3) {
+        x3 = grp % nx3;
+        y3 = grp / nx3;  // TZ == 8: a single level-3 slice per tile
+        z3 = 0;
+      } else {
+        const int nx4 = nx3 >> 1;
+        const int c4 = grp >> 3, ch = grp & 7;
+        const int x4 = c4 % nx4, y4 = c4 / nx4;  // TZ == 16: a single level-4 slice per tile
+        x3 = 2 * x4 + (ch & 1);
+        y3 = 2 * y4 + ((ch >> 1) & 1);
+        z3 = ch >> 2;
       }
+      c_z2 = 2 * z3 + (q >> 1);
+      c_y2 = 2 * y3 + (q & 1);
+      c_x2 = 2 * x3;
+      // first level-1 child row (z1 = 2 z2, y1 = 2 y2), x1 = 2 x2 .. 2 x2 + 3
+      c_s1 = s1a + 2u * (uint32_t)(((2 * c_z2) * rows_u + 2 * c_y2) * s1_row + 2 * c_x2);
+    }
+  }
+  __syncthreads();
+
+  const bool want0 = a.lv[0].out != nullptr, want1 = a.lv[1].out != nullptr;
+  int since_flush = 0;
+  int tx_i = 0, ty_i = 0, tz_i = 0;
+  {
+    const int rest = t_begin / g.tiles_x;
+    tx_i = t_begin - rest * g.tiles_x;
+    ty_i = rest % g.tiles_y;
+    tz_i = rest / g.tiles_y;
+  }
+  int k = 0;
+  for (int tile = t_begin; tile < t_end; tile++, k++) {
+    const int stage = k % NST;
+    const uint32_t sbase = stage0 + (uint32_t)stage * LY::STAGE_BYTES;
+    const int x0 = tx_i * xw, y0 = ty_i * g.ty, z0 = tz_i * TZ;
+    mbar_wait(bar0 + 8u * stage, (uint32_t)((k / NST) & 1));
+    uint16_t* s1k = s1 + (k & 1) * (LY::S1_BYTES / 2);
+    const uint32_t s1off = (uint32_t)(k & 1) * LY::S1_BYTES;
 
 #pragma unroll
-      for (int i = 0; i < kBatch; i++) {
-        if (!ok[i]) continue;
-        const int s = bt + i;
-        const int xu = uxu[s], yr = uyr[s], zr = uzr[s];
-        const int x = x0 + xu * UXW, y = y0 + yr * UZ, z = z0 + zr * UZ;
-        uint32_t acc[L1PU];
+    for (int i = 0; i < UPT; i++) {
+      const int xu = uxu[i], yr = uyr[i], zr = uzr[i];
+      const int x = x0 + xu * UXW, y = y0 + yr * UZ, z = z0 + zr * UZ;
+      if (zr >= TZ / UZ || x >= g.nx || y >= g.ny) continue;
+      uint32_t acc[L1PU];
 #pragma unroll
-        for (int j = 0; j < L1PU; j++) acc[j] = 0;
+      for (int j = 0; j < L1PU; j++) acc[j] = 0;
 #pragma unroll
-        for (int r2 = 0; r2 < ROWS; r2++) {
-          uint32_t o[UXW];
-          row_atomics<T, LAYOUT>(q[i][r2], lb, o);
-          if (a.lv[0].out) {  // level 0: the filtered voxels themselves
-            uint8_t* dst = a.lv[0].out + level_offset(a.lv[0], z + r2 / UZ, y + r2 % UZ, x);
+      for (int r2 = 0; r2 < ROWS; r2 += (L >= 1 ? 2 : 1)) {
+        // two rows at a time: acc += o_r[2j] + o_r[2j+1] + o_r'[2j] + o_r'[2j+1] as 3-input adds
+        uint32_t o[2][UXW];
+#pragma unroll
+        for (int h = 0; h < (L >= 1 ? 2 : 1); h++) {
+          const int rr = r2 + h;
+          const uint4 q = lds128(sbase + uso[i] + (rr / UZ) * row_dz + (rr % UZ) * row_dy);
+          row_atomics<T>(q, lb, o[h]);
+          if (want0) {  // level 0: the filtered voxels themselves
+            uint8_t* dst = a.lv[0].out + level_offset(a.lv[0], z + rr / UZ, y + rr % UZ, x);
             uint32_t pk[UXW / 4];
 #pragma unroll
-            for (int k = 0; k < UXW / 4; k++)
-              pk[k] = __byte_perm(__byte_perm(o[4 * k], o[4 * k + 1], 0x0040),
-                                  __byte_perm(o[4 * k + 2], o[4 * k + 3], 0x0040), 0x5410);
+            for (int kk = 0; kk < UXW / 4; kk++)
+              pk[kk] = __byte_perm(__byte_perm(o[h][4 * kk], o[h][4 * kk + 1], 0x0040),
+                                   __byte_perm(o[h][4 * kk + 2], o[h][4 * kk + 3], 0x0040), 0x5410);
             if constexpr (UXW == 16) {
               if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)
                 *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -254,124 +328,220 @@ __global__ void __launch_bounds__(kPvThreads, MINB) preview_kernel(const PvArgs 
               store8(dst, pk[0], pk[1]);
             }
           }
-          if constexpr (L >= 1) {
-#pragma unroll
-            for (int j = 0; j < L1PU; j++) acc[j] += o[2 * j] + o[2 * j + 1];
-          }
         }
         if constexpr (L >= 1) {
-          uint32_t sum[L1PU];
 #pragma unroll
-          for (int j = 0; j < L1PU; j++) sum[j] = acc[j] & 0xFFFu;  // sum of f over the 2x2x2 cell (<= 2040)
-          if (a.lv[1].out) {
-            uint32_t pk[L1PU / 4];
-#pragma unroll
-            for (int k = 0; k < L1PU / 4; k++)
-              pk[k] = ((sum[4 * k] + 4) >> 3) | (((sum[4 * k + 1] + 4) >> 3) << 8) |
-                      (((sum[4 * k + 2] + 4) >> 3) << 16) | (((sum[4 * k + 3] + 4) >> 3) << 24);
-            uint8_t* dst = a.lv[1].out + level_offset(a.lv[1], z >> 1, y >> 1, x >> 1);
-            if constexpr (L1PU == 8) {
-              store8(dst, pk[0], pk[1]);
-            } else {
-              if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = pk[0];
-              else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(pk[0] >> (8 * b));
-            }
-          }
-          if constexpr (L >= 2) {
-            // s1 layout [zr][yr][x1], x1 = xu*L1PU + j
-            uint16_t* d = s1 + ((zr * rows_u + yr) * g.txu + xu) * L1PU;
-            if constexpr (L1PU == 8)
-              *reinterpret_cast<uint4*>(d) = make_uint4(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16),
-                                                        sum[4] | (sum[5] << 16), sum[6] | (sum[7] << 16));
-            else
-              *reinterpret_cast<uint2*>(d) = make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
-          }
+          for (int j = 0; j < L1PU; j++) acc[j] = acc[j] + (o[0][2 * j] + o[0][2 * j + 1]) + (o[1][2 * j] + o[1][2 * j + 1]);
         }
       }
-    }  // batch loop
-
-    // ---- levels 2..L from shared memory ----------------------------------------
-    if constexpr (L >= 2) {
-      __syncthreads();
+      if constexpr (L >= 1) {
+        // pack the 12-bit sums of f (<= 2040) two per word: the s1 layout
+        uint32_t pr[L1PU / 2];
 #pragma unroll
-      for (int l = 2; l <= L; l++) {
-        const int cy = g.ty >> (l - 1), cx = xw >> (l - 1);  // child dims (y, x)
-        const int lnx = (int)(g.nx >> l), lny = (int)(g.ny >> l);
-        const int shift = 3 * l;
-        uint32_t* dsts = (l == 2) ? s2 : s3;
-        const uint32_t* srcs = (l == 3) ? s2 : s3;
-        const bool want = a.lv[l].out != nullptr;
+        for (int j = 0; j < L1PU / 2; j++) pr[j] = __byte_perm(acc[2 * j], acc[2 * j + 1], 0x5410) & 0x0FFF0FFFu;
+        if (want1) {
+          uint32_t pk[L1PU / 4];
 #pragma unroll
-        for (int k = 0; k < kCellSlots; k++) {
-          if (l > 2 && k > 0) break;
-          const int code = cslot[(l == 2 ? k : kCellSlots + l - 3) * kPvThreads + threadIdx.x];
-          if (code < 0) continue;
-          const int xq = code & 0xFFF, yq = (code >> 12) & 0xFFF, zq = code >> 24;
-          const int gx = (x0 >> l) + xq, gy = (y0 >> l) + yq;
-          if (gx >= lnx || gy >= lny) continue;
-          uint32_t sum = 0;
-#pragma unroll
-          for (int dz = 0; dz < 2; dz++)
-#pragma unroll
-            for (int dy = 0; dy < 2; dy++) {
-              const int base = ((2 * zq + dz) * cy + (2 * yq + dy)) * cx + 2 * xq;
-              if (l == 2) {
-                const uint32_t pair = *reinterpret_cast<const uint32_t*>(s1 + base);
-                sum += (pair & 0xFFFFu) + (pair >> 16);
-              } else {
-                sum += srcs[base] + srcs[base + 1];
-              }
-            }
-          if (l < L) dsts[threadIdx.x + kPvThreads * k] = sum;
-          if (want)
-            a.lv[l].out[level_offset(a.lv[l], (z0 >> l) + zq, gy, gx)] =
-                (uint8_t)((sum + (1u << (shift - 1))) >> shift);
+          for (int kk = 0; kk < L1PU / 4; kk++)
+            pk[kk] = __byte_perm(round_l1_pair(pr[2 * kk]), round_l1_pair(pr[2 * kk + 1]), 0x6420);
+          uint8_t* dst = a.lv[1].out + level_offset(a.lv[1], z >> 1, y >> 1, x >> 1);
+          if constexpr (L1PU == 8) {
+            store8(dst, pk[0], pk[1]);
+          } else {
+            if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = pk[0];
+            else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(pk[0] >> (8 * b));
+          }
         }
-        __syncthreads();
+        if constexpr (L >= 2) {
+          // s1 layout [zr][yr][x1], x1 = xu*L1PU + j
+          uint16_t* d = s1k + (zr * rows_u + yr) * s1_row + xu * L1PU;
+          if constexpr (L1PU == 8) *reinterpret_cast<uint4*>(d) = make_uint4(pr[0], pr[1], pr[2], pr[3]);
+          else *reinterpret_cast<uint2*>(d) = make_uint2(pr[0], pr[1]);
+        }
+      }
+    }
+
+    // every thread is done with this stage (and s1 is complete): refill it
+    __syncthreads();
+    if (threadIdx.x == 0 && tile + NST < t_end) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+      issue(tile + NST, stage);
+    }
+
+    // ---- levels 2..L from the level-1 sums -------------------------------------------
+    if constexpr (L == 2) {
+      const int nx2 = xw >> 2, ny2 = g.ty >> 2;
+      const int cells = ny2 * nx2;  // TZ == 4: one level-2 slice per tile
+      const bool want2 = a.lv[2].out != nullptr;
+      for (int c = threadIdx.x; c < cells; c += THREADS) {
+        const int x2 = c % nx2, y2 = c / nx2;
+        const int gx = (x0 >> 2) + x2, gy = (y0 >> 2) + y2;
+        if (gx >= (g.nx >> 2) || gy >= (g.ny >> 2)) continue;
+        uint32_t sum = 0;
+#pragma unroll
+        for (int ez = 0; ez < 2; ez++)
+#pragma unroll
+          for (int ey = 0; ey < 2; ey++) {
+            const uint32_t pair = *reinterpret_cast<const uint32_t*>(s1k + (ez * rows_u + 2 * y2 + ey) * s1_row + 2 * x2);
+            sum += (pair & 0xFFFFu) + (pair >> 16);
+          }
+        if (want2) a.lv[2].out[level_offset(a.lv[2], z0 >> 2, gy, gx)] = (uint8_t)((sum + 32) >> 6);
+      }
+    } else if constexpr (L >= 3) {
+      uint32_t sa = 0, sb = 0;  // the two level-2 children of this lane
+      if (c_x2 >= 0) {
+#pragma unroll
+        for (int ez = 0; ez < 2; ez++)
+#pragma unroll
+          for (int ey = 0; ey < 2; ey++) {
+            uint32_t h0, h1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(h0), "=r"(h1)
+                         : "r"(c_s1 + s1off + 2u * (uint32_t)((ez * rows_u + ey) * s1_row)));
+            sa += (h0 & 0xFFFFu) + (h0 >> 16);
+            sb += (h1 & 0xFFFFu) + (h1 >> 16);
+          }
+        const int gx = (x0 >> 2) + c_x2, gy = (y0 >> 2) + c_y2;
+        if (a.lv[2].out != nullptr && gx < (g.nx >> 2) && gy < (g.ny >> 2)) {
+          uint8_t* dst = a.lv[2].out + level_offset(a.lv[2], (z0 >> 2) + c_z2, gy, gx);
+          const uint32_t v = ((sa + 32) >> 6) | (((sb + 32) >> 6) << 8);
+          if ((reinterpret_cast<uintptr_t>(dst) & 1) == 0) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)v;
+          else { dst[0] = (uint8_t)v; dst[1] = (uint8_t)(v >> 8); }
+        }
+      }
+      uint32_t s3v = sa + sb;
+      s3v += __shfl_xor_sync(0xFFFFFFFFu, s3v, 1);
+      s3v += __shfl_xor_sync(0xFFFFFFFFu, s3v, 2);
+      if (c_x2 >= 0 && (threadIdx.x & 3) == 0) {
+        const int gx = (x0 >> 3) + (c_x2 >> 1), gy = (y0 >> 3) + (c_y2 >> 1);
+        if (a.lv[3].out != nullptr && gx < (g.nx >> 3) && gy < (g.ny >> 3))
+          a.lv[3].out[level_offset(a.lv[3], (z0 >> 3) + (c_z2 >> 1), gy, gx)] = (uint8_t)((s3v + 256) >> 9);
+      }
+      if constexpr (L == 4) {
+        uint32_t s4v = s3v;
+        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 4);
+        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 8);
+        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 16);
+        if (c_x2 >= 0 && lane == 0) {
+          const int gx = (x0 >> 4) + (c_x2 >> 2), gy = (y0 >> 4) + (c_y2 >> 2);
+          if (a.lv[4].out != nullptr && gx < (g.nx >> 4) && gy < (g.ny >> 4))
+            a.lv[4].out[level_offset(a.lv[4], (z0 >> 4), gy, gx)] = (uint8_t)((s4v + 2048) >> 12);
+        }
       }
     }
 
     if (++since_flush == g.flush_tiles) {
       since_flush = 0;
-      flush_counts<T, LAYOUT>(hs, a.hist);
+      flush_counts<T>(hs, a.hist, THREADS);
+    }
+    // next tile (row-major: x fastest)
+    if (++tx_i == g.tiles_x) {
+      tx_i = 0;
+      if (++ty_i == g.tiles_y) { ty_i = 0; ++tz_i; }
     }
   }
-  flush_counts<T, LAYOUT>(hs, a.hist);
+  flush_counts<T>(hs, a.hist, THREADS);
 }
 
-template <typename T, int LAYOUT>
-static size_t smem_bytes(int L) {
-  size_t b = (size_t)Table<T, LAYOUT>::WORDS * 4;
-  if (L >= 2) {
-    const size_t l1 = (size_t)kMaxUnits * (Vox<T>::UXW / 2);
-    b += l1 * 2 + (l1 / 8) * 4 + (l1 / 64) * 4 + 16 + (kCellSlots + 2) * kPvThreads * 4;
+template <typename T, int L, int NST, int MAXU, int THREADS>
+static constexpr size_t smem_bytes() {
+  using LY = PvLayout<T, L, MAXU>;
+  static_assert(L < 3 || MAXU * LY::L1PU <= 16 * THREADS, "level-3 lane groups must fit in the CTA");
+  return (size_t)NST * LY::STAGE_BYTES + LY::HIST_BYTES + 2 * LY::S1_BYTES + NST * 8;
+}
+
+// ---- TMA descriptor ---------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled encode_fn() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  });
+  return fn;
+}
+
+template <typename T>
+static int make_tmap(CUtensorMap* map, const T* vol, const PvGeom& g, int tz) {
+  PFN_cuTensorMapEncodeTiled fn = encode_fn();
+  CTP_REQUIRE(fn != nullptr, CTP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.nx * sizeof(T), (cuuint64_t)g.nx * g.ny * sizeof(T)};
+  const cuuint32_t box[3] = {(cuuint32_t)g.box_x, (cuuint32_t)g.ty, (cuuint32_t)tz};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                  const_cast<T*>(vol), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CTP_REQUIRE(r == CUDA_SUCCESS, CTP_E_CUDA, "cuTensorMapEncodeTiled failed (%d): box (%d,%d,%d)", (int)r, g.box_x,
+              g.ty, tz);
+  return CTP_OK;
+}
+
+// tile geometry for at most `maxu` units per tile; boxes of <= 256 x-elements
+template <typename T>
+static void plan_tiles(PvGeom& g, int nlev, int maxu) {
+  constexpr int UXW = Vox<T>::UXW;
+  const int uz = nlev == 0 ? 1 : 2;
+  const int tz = 1 << nlev;
+  const int64_t blk = 1LL << nlev;
+  const int64_t xu_total = g.nx / UXW;
+  const int64_t urows_per_block = (int64_t)(tz / uz) * (blk / uz);  // unit rows in a 2^L x 2^L block
+  if (xu_total * urows_per_block <= maxu && xu_total * UXW <= kBoxX) {
+    g.txu = (int)xu_total;
+    int64_t ky = maxu / (xu_total * urows_per_block);
+    const int64_t ky_max = (g.ny + blk - 1) / blk;
+    if (ky > ky_max) ky = ky_max;
+    if (ky * blk > 256) ky = 256 / blk;  // TMA box rows <= 256
+    if (ky < 1) ky = 1;
+    g.ty = (int)(ky * blk);
+  } else {
+    int64_t txu = maxu / urows_per_block;
+    if (txu > xu_total) txu = xu_total;
+    const int64_t box_u = kBoxX / UXW;  // a tile wider than one box is whole boxes
+    if (txu > box_u) txu = (txu / box_u) * box_u;
+    g.txu = (int)txu;
+    g.ty = (int)blk;
   }
-  return b;
+  const int xw = g.txu * UXW;
+  g.box_x = xw <= kBoxX ? xw : kBoxX;
+  g.nboxes = (xw + g.box_x - 1) / g.box_x;
+  g.box_bytes = (uint32_t)g.box_x * g.ty * tz * sizeof(T);
+  g.tiles_x = (int)((xu_total + g.txu - 1) / g.txu);
+  g.tiles_y = (g.ny + g.ty - 1) / g.ty;
 }
 
-template <typename T, int L, int MINB, int BATCH, int LAYOUT>
-static int launch_v(PvArgs a, cudaStream_t st) {
-  const size_t sm = smem_bytes<T, LAYOUT>(L);
-  auto kern = preview_kernel<T, L, MINB, BATCH, LAYOUT>;
-  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+template <typename T, int L, int THREADS, int NST, int MAXU>
+static int launch_v(PvArgs a, const T* vol, cudaStream_t st) {
+  plan_tiles<T>(a.g, L, MAXU);
+  const int64_t n_tiles = (int64_t)a.g.tiles_x * a.g.tiles_y * (a.g.nz >> L);
+  CTP_REQUIRE(n_tiles < (1LL << 31), CTP_E_INVALID, "preview: too many tiles");
+  a.g.n_tiles = (int)n_tiles;
   // a counter word gains at most this many counts per tile
   constexpr int UZ = L == 0 ? 1 : 2;
   const int64_t vox_per_unit = (int64_t)Vox<T>::UXW * UZ * UZ;
-  int64_t per_tile;
-  if (sizeof(T) == 2) per_tile = (int64_t)kMaxUnits * vox_per_unit;                // whole CTA
-  else if (LAYOUT == kLaneCols) per_tile = 8LL * kUnitsPerThread * vox_per_unit;    // one lane of 8 warps
-  else per_tile = 32LL * kUnitsPerThread * vox_per_unit;                            // one warp
+  const int64_t per_tile = sizeof(T) == 2 ? (int64_t)MAXU * vox_per_unit                    // whole CTA
+                                          : (int64_t)(THREADS / 32) * (MAXU / THREADS) * vox_per_unit;  // a lane column
   a.g.flush_tiles = (int)(kCountCap / per_tile);
   if (a.g.flush_tiles < 1) a.g.flush_tiles = 1;
-  int grid = num_sms() * MINB;
+  CUtensorMap map;
+  int rc = make_tmap<T>(&map, vol, a.g, 1 << L);
+  if (rc != CTP_OK) return rc;
+  constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
+  static_assert(sm <= 227 * 1024, "shared memory budget");
+  auto kern = preview_kernel<T, L, THREADS, NST, MAXU>;
+  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int grid = num_sms();
   if (a.g.n_tiles < grid) grid = a.g.n_tiles;
-  kern<<<grid, kPvThreads, sm, st>>>(a);
+  kern<<<grid, THREADS, sm, st>>>(map, a);
   CTP_CUDA_CHECK_LAUNCH("preview_kernel");
   return CTP_OK;
 }
 
 // Launch-shape variants, selectable with CTP_PREVIEW_VARIANT for tuning
-// (tools/prof_preview.py); the default was the fastest measured on B200.
+// (tools/prof_preview.py); the default is the fastest measured on B200.
 static int preview_variant() {
   static int v = -1;
   if (v < 0) {
@@ -382,17 +552,11 @@ static int preview_variant() {
 }
 
 template <typename T, int L>
-static int launch_l(const PvArgs& a, cudaStream_t st) {
-  if constexpr (sizeof(T) == 1) {
-    switch (preview_variant()) {
-      case 1: return launch_v<T, L, 3, 1, kLaneCols>(a, st);
-      case 2: return launch_v<T, L, 2, 2, kWarpPriv>(a, st);
-      case 3: return launch_v<T, L, 3, 1, kWarpPriv>(a, st);
-      case 4: return launch_v<T, L, 4, 1, kLaneCols>(a, st);
-      default: return launch_v<T, L, 2, 2, kLaneCols>(a, st);
-    }
-  } else {
-    return launch_v<T, L, 2, 2, kLaneCols>(a, st);
+static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
+  switch (preview_variant()) {
+    case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
+    case 3: return launch_v<T, L, 256, 4, 512>(a, vol, st);
+    default: return launch_v<T, L, 512, 2, 1024>(a, vol, st);
   }
 }
 
@@ -419,47 +583,23 @@ static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_
     CTP_REQUIRE(levels[l].out == nullptr, CTP_E_INVALID, "preview: level %d requested above nlev %d", l, nlev);
 
   PvArgs a;
-  a.vol = vol;
   a.lut = lut;
   a.hist = reinterpret_cast<unsigned long long*>(hist);
   for (int l = 0; l < CTP_MAX_LEVELS; l++) {
     a.lv[l] = make_dst(levels[l], nx >> l, ny >> l, z_base >> l);
     if (l > nlev) a.lv[l].out = nullptr;
   }
-  // tile geometry: <= kMaxUnits units
-  const int uz = nlev == 0 ? 1 : 2;
-  const int tz = 1 << nlev;
-  const int64_t xu_total = nx / UXW;
-  const int64_t urows_per_block = (int64_t)(tz / uz) * (blk / uz);  // unit rows in a 2^L x 2^L block
-  PvGeom& g = a.g;
-  g.nx = nx; g.ny = ny; g.nz = nz; g.z_base = z_base;
-  if (xu_total * urows_per_block <= kMaxUnits) {
-    g.txu = (int)xu_total;
-    int64_t ky = kMaxUnits / (xu_total * urows_per_block);
-    const int64_t ky_max = (ny + blk - 1) / blk;
-    if (ky > ky_max) ky = ky_max;
-    if (ky < 1) ky = 1;
-    g.ty = (int)(ky * blk);
-  } else {
-    g.txu = (int)(kMaxUnits / urows_per_block);
-    g.ty = (int)blk;
-  }
-  const int64_t tiles_x = (xu_total + g.txu - 1) / g.txu;
-  const int64_t tiles_y = (ny + g.ty - 1) / g.ty;
-  const int64_t n_tiles = tiles_x * tiles_y * (nz / tz);
-  CTP_REQUIRE(n_tiles < (1LL << 31), CTP_E_INVALID, "preview: too many tiles");
-  g.tiles_x = (int)tiles_x;
-  g.tiles_y = (int)tiles_y;
-  g.n_tiles = (int)n_tiles;
-  g.flush_tiles = 1;
+  a.g.nx = (int)nx;
+  a.g.ny = (int)ny;
+  a.g.nz = (int)nz;
 
   cudaStream_t st = as_stream(stream);
   switch (nlev) {
-    case 0: return launch_l<T, 0>(a, st);
-    case 1: return launch_l<T, 1>(a, st);
-    case 2: return launch_l<T, 2>(a, st);
-    case 3: return launch_l<T, 3>(a, st);
-    default: return launch_l<T, 4>(a, st);
+    case 0: return launch_l<T, 0>(a, vol, st);
+    case 1: return launch_l<T, 1>(a, vol, st);
+    case 2: return launch_l<T, 2>(a, vol, st);
+    case 3: return launch_l<T, 3>(a, vol, st);
+    default: return launch_l<T, 4>(a, vol, st);
   }
 }
 
