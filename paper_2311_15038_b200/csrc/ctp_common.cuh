@@ -52,17 +52,28 @@ struct LevelDst {
   uint8_t* out;
   int32_t layout;
   int32_t s, grid, atlas_dim;
-  int32_t gshift;          // log2(grid) when grid is a power of two, else -1
+  int32_t gshift;          // log2(grid) when grid is a power of two, else -1 (dense: 0)
   int32_t z_off;           // added to the slab-local z: global slice index for atlases, 0 for dense
   int64_t nx, ny;          // level dims (x, y) for the dense layout
-  int64_t map_bytes;       // atlas_dim^2
+  int64_t map_bytes;       // atlas_dim^2 (dense: bytes per slice)
+  int32_t row;             // bytes between rows (atlas_dim, or nx for dense)
+  int32_t cell_row;        // s * atlas_dim (dense: 0)
+  int32_t cell_col;        // s (dense: 0)
+  int32_t gmask;           // grid - 1 (dense: 0)
 };
 
 // Byte offset of level voxel (z, y, x), z slab-local (z_off makes it the
 // global slice index for atlases).  Atlas: slicemap.py:79-85 (slice_cell) and the mosaic of
 // slicemap.py:139-140: atlas[m][cy*s + y, cx*s + x] = cube[m*g^2 + cy*g + cx, y, x].
+// POW2: power-of-two grid -- branch-free shifts/masks; a dense level is the
+// degenerate 1x1-grid atlas whose "maps" are its slices.
+template <bool POW2 = false>
 __device__ __forceinline__ int64_t level_offset(const LevelDst& d, int z, int y, int x) {
   z += d.z_off;
+  if (POW2) {
+    return (int64_t)(z >> (2 * d.gshift)) * d.map_bytes +
+           (int64_t)(((z >> d.gshift) & d.gmask) * d.cell_row + (z & d.gmask) * d.cell_col + y * d.row + x);
+  }
   if (d.layout == CTP_LAYOUT_ATLAS) {
     int m, cy, cx;
     if (d.gshift >= 0) {
@@ -98,12 +109,6 @@ __device__ __forceinline__ void store8(uint8_t* p, uint32_t lo, uint32_t hi) {
 
 inline LevelDst make_dst(const ctp_level_out& lo, int64_t nx, int64_t ny, int64_t z_off_atlas = 0) {
   LevelDst d;
-  d.z_off = lo.layout == CTP_LAYOUT_ATLAS ? (int32_t)z_off_atlas : 0;
-  d.gshift = -1;
-  if (lo.grid > 0 && (lo.grid & (lo.grid - 1)) == 0) {
-    d.gshift = 0;
-    while ((1 << d.gshift) < lo.grid) d.gshift++;
-  }
   d.out = lo.out;
   d.layout = lo.layout;
   d.s = lo.s;
@@ -111,9 +116,31 @@ inline LevelDst make_dst(const ctp_level_out& lo, int64_t nx, int64_t ny, int64_
   d.atlas_dim = lo.atlas_dim;
   d.nx = nx;
   d.ny = ny;
-  d.map_bytes = (int64_t)lo.atlas_dim * lo.atlas_dim;
+  if (lo.layout == CTP_LAYOUT_ATLAS) {
+    d.z_off = (int32_t)z_off_atlas;
+    d.gshift = -1;
+    if (lo.grid > 0 && (lo.grid & (lo.grid - 1)) == 0) {
+      d.gshift = 0;
+      while ((1 << d.gshift) < lo.grid) d.gshift++;
+    }
+    d.map_bytes = (int64_t)lo.atlas_dim * lo.atlas_dim;
+    d.row = lo.atlas_dim;
+    d.cell_row = lo.s * lo.atlas_dim;
+    d.cell_col = lo.s;
+    d.gmask = lo.grid - 1;
+  } else {  // dense level == 1x1-grid atlas of slices
+    d.z_off = 0;
+    d.gshift = 0;
+    d.map_bytes = nx * ny;
+    d.row = (int32_t)nx;
+    d.cell_row = 0;
+    d.cell_col = 0;
+    d.gmask = 0;
+  }
   return d;
 }
+
+inline bool dst_is_pow2(const LevelDst& d) { return d.out == nullptr || d.gshift >= 0; }
 
 // Host-side validation of an atlas descriptor (slicemap.py:52-61) against
 // the level dims it will receive (_pad_to_cube: every dim <= s).

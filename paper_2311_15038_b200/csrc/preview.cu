@@ -163,7 +163,7 @@ struct PvLayout {
 // (sum + 4) >> 3 of two packed 12-bit level-1 sums, as two bytes in 16-bit lanes
 __device__ __forceinline__ uint32_t round_l1_pair(uint32_t p) { return ((p + 0x00040004u) >> 3) & 0x00FF00FFu; }
 
-template <typename T, int L, int THREADS, int NST, int MAXU>
+template <typename T, int L, int THREADS, int NST, int MAXU, bool WANT0, bool POW2>
 __global__ void __launch_bounds__(THREADS, 1)
     preview_kernel(const __grid_constant__ CUtensorMap tmap, const PvArgs a) {
   using LY = PvLayout<T, L, MAXU>;
@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
-  const bool want0 = a.lv[0].out != nullptr, want1 = a.lv[1].out != nullptr;
+  constexpr bool want0 = WANT0;
+  const bool want1 = a.lv[1].out != nullptr;
   int since_flush = 0;
   int tx_i = 0, ty_i = 0, tz_i = 0;
   {
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint4 q = lds128(sbase + uso[i] + (rr / UZ) * row_dz + (rr % UZ) * row_dy);
           row_atomics<T>(q, lb, o[h]);
           if (want0) {  // level 0: the filtered voxels themselves
-            uint8_t* dst = a.lv[0].out + level_offset(a.lv[0], z + rr / UZ, y + rr % UZ, x);
+            uint8_t* dst = a.lv[0].out + level_offset<POW2>(a.lv[0], z + rr / UZ, y + rr % UZ, x);
             uint32_t pk[UXW / 4];
 #pragma unroll
             for (int kk = 0; kk < UXW / 4; kk++)
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < L1PU / 4; kk++)
             pk[kk] = __byte_perm(round_l1_pair(pr[2 * kk]), round_l1_pair(pr[2 * kk + 1]), 0x6420);
-          uint8_t* dst = a.lv[1].out + level_offset(a.lv[1], z >> 1, y >> 1, x >> 1);
+          uint8_t* dst = a.lv[1].out + level_offset<POW2>(a.lv[1], z >> 1, y >> 1, x >> 1);
           if constexpr (L1PU == 8) {
             store8(dst, pk[0], pk[1]);
           } else {
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t pair = *reinterpret_cast<const uint32_t*>(s1k + (ez * rows_u + 2 * y2 + ey) * s1_row + 2 * x2);
             sum += (pair & 0xFFFFu) + (pair >> 16);
           }
-        if (want2) a.lv[2].out[level_offset(a.lv[2], z0 >> 2, gy, gx)] = (uint8_t)((sum + 32) >> 6);
+        if (want2) a.lv[2].out[level_offset<POW2>(a.lv[2], z0 >> 2, gy, gx)] = (uint8_t)((sum + 32) >> 6);
       }
     } else if constexpr (L >= 3) {
       uint32_t sa = 0, sb = 0;  // the two level-2 children of this lane
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         const int gx = (x0 >> 2) + c_x2, gy = (y0 >> 2) + c_y2;
         if (a.lv[2].out != nullptr && gx < (g.nx >> 2) && gy < (g.ny >> 2)) {
-          uint8_t* dst = a.lv[2].out + level_offset(a.lv[2], (z0 >> 2) + c_z2, gy, gx);
+          uint8_t* dst = a.lv[2].out + level_offset<POW2>(a.lv[2], (z0 >> 2) + c_z2, gy, gx);
           const uint32_t v = ((sa + 32) >> 6) | (((sb + 32) >> 6) << 8);
           if ((reinterpret_cast<uintptr_t>(dst) & 1) == 0) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)v;
           else { dst[0] = (uint8_t)v; dst[1] = (uint8_t)(v >> 8); }
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (c_x2 >= 0 && (threadIdx.x & 3) == 0) {
         const int gx = (x0 >> 3) + (c_x2 >> 1), gy = (y0 >> 3) + (c_y2 >> 1);
         if (a.lv[3].out != nullptr && gx < (g.nx >> 3) && gy < (g.ny >> 3))
-          a.lv[3].out[level_offset(a.lv[3], (z0 >> 3) + (c_z2 >> 1), gy, gx)] = (uint8_t)((s3v + 256) >> 9);
+          a.lv[3].out[level_offset<POW2>(a.lv[3], (z0 >> 3) + (c_z2 >> 1), gy, gx)] = (uint8_t)((s3v + 256) >> 9);
       }
       if constexpr (L == 4) {
         uint32_t s4v = s3v;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (c_x2 >= 0 && lane == 0) {
           const int gx = (x0 >> 4) + (c_x2 >> 2), gy = (y0 >> 4) + (c_y2 >> 2);
           if (a.lv[4].out != nullptr && gx < (g.nx >> 4) && gy < (g.ny >> 4))
-            a.lv[4].out[level_offset(a.lv[4], (z0 >> 4), gy, gx)] = (uint8_t)((s4v + 2048) >> 12);
+            a.lv[4].out[level_offset<POW2>(a.lv[4], (z0 >> 4), gy, gx)] = (uint8_t)((s4v + 2048) >> 12);
         }
       }
     }
@@ -513,6 +514,17 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
   g.tiles_y = (g.ny + g.ty - 1) / g.ty;
 }
 
+template <typename T, int L, int THREADS, int NST, int MAXU, bool WANT0, bool POW2>
+static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
+  constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
+  static_assert(sm <= 227 * 1024, "shared memory budget");
+  auto kern = preview_kernel<T, L, THREADS, NST, MAXU, WANT0, POW2>;
+  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  kern<<<grid, THREADS, sm, st>>>(map, a);
+  CTP_CUDA_CHECK_LAUNCH("preview_kernel");
+  return CTP_OK;
+}
+
 template <typename T, int L, int THREADS, int NST, int MAXU>
 static int launch_v(PvArgs a, const T* vol, cudaStream_t st) {
   plan_tiles<T>(a.g, L, MAXU);
@@ -529,15 +541,17 @@ static int launch_v(PvArgs a, const T* vol, cudaStream_t st) {
   CUtensorMap map;
   int rc = make_tmap<T>(&map, vol, a.g, 1 << L);
   if (rc != CTP_OK) return rc;
-  constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
-  static_assert(sm <= 227 * 1024, "shared memory budget");
-  auto kern = preview_kernel<T, L, THREADS, NST, MAXU>;
-  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int grid = num_sms();
   if (a.g.n_tiles < grid) grid = a.g.n_tiles;
-  kern<<<grid, THREADS, sm, st>>>(map, a);
-  CTP_CUDA_CHECK_LAUNCH("preview_kernel");
-  return CTP_OK;
+  bool pow2 = true;
+  for (int l = 0; l <= L; l++) pow2 = pow2 && dst_is_pow2(a.lv[l]);
+  const bool want0 = a.lv[0].out != nullptr;
+  if (pow2) {
+    if (want0) return launch_k<T, L, THREADS, NST, MAXU, true, true>(a, map, grid, st);
+    return launch_k<T, L, THREADS, NST, MAXU, false, true>(a, map, grid, st);
+  }
+  if (want0) return launch_k<T, L, THREADS, NST, MAXU, true, false>(a, map, grid, st);
+  return launch_k<T, L, THREADS, NST, MAXU, false, false>(a, map, grid, st);
 }
 
 // Launch-shape variants, selectable with CTP_PREVIEW_VARIANT for tuning
@@ -555,7 +569,6 @@ template <typename T, int L>
 static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
   switch (preview_variant()) {
     case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
-    case 3: return launch_v<T, L, 256, 4, 512>(a, vol, st);
     default: return launch_v<T, L, 512, 2, 1024>(a, vol, st);
   }
 }
