@@ -17,6 +17,7 @@
 // mode (v = -1: not > 0, not >= threshold, not > max, not composited).
 #include "ctp_common.cuh"
 #include <math.h>
+#include <stdlib.h>
 
 namespace ctp {
 
@@ -29,7 +30,13 @@ struct ViewDev {
   int32_t steps, mode, threshold, channels;
   double gain;
   float tf[4][5];
+  double slope[3][4];  // (c_{j+1} - c_j) / (x_{j+1} - x_j) per segment and channel
   float early_stop;
+};
+
+constexpr int kMaxViews = 64;
+struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per launch
+  ViewDev v[kMaxViews];
 };
 
 template <typename R>
@@ -86,7 +93,7 @@ __device__ __forceinline__ void clip_axis(double o, double d, double half, doubl
 
 // piecewise-linear RGBA transfer function (frozen in oracle/ctp_oracle.py tf_eval)
 template <typename R>
-__device__ __forceinline__ void tf_eval(const float (*tf)[5], R x, R* c) {
+__device__ __forceinline__ void tf_eval(const float (*tf)[5], const double (*slope)[4], R x, R* c) {
   if (x <= (R)tf[0][0]) {
     for (int q = 0; q < 4; q++) c[q] = (R)tf[0][q + 1];
     return;
@@ -96,12 +103,9 @@ __device__ __forceinline__ void tf_eval(const float (*tf)[5], R x, R* c) {
     return;
   }
   int j = (x < (R)tf[1][0]) ? 0 : ((x < (R)tf[2][0]) ? 1 : 2);
-  const R x0 = (R)tf[j][0], x1 = (R)tf[j + 1][0];
+  const R x0 = (R)tf[j][0];
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const R c0 = (R)tf[j][q + 1], c1 = (R)tf[j + 1][q + 1];
-    c[q] = c0 + (x - x0) * ((c1 - c0) / (x1 - x0));
-  }
+  for (int q = 0; q < 4; q++) c[q] = (R)tf[j][q + 1] + (x - x0) * (R)slope[j][q];
 }
 
 template <typename R>
@@ -113,13 +117,13 @@ __device__ __forceinline__ uint8_t to_u8_unit(R v) {  // floor(min(v, 1) * 255 +
 
 template <typename R>
 __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__ vox, int nx, int ny, int nz,
-                                                     const ViewDev* __restrict__ views, int dim, int row0, int row1,
-                                                     uint8_t* __restrict__ out) {
+                                                     const __grid_constant__ ViewBatch views, int dim, int row0,
+                                                     int row1, uint8_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
   const int view = blockIdx.z;
   if (i >= dim || j >= row1) return;
-  const ViewDev& V = views[view];
+  const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
   const int ch = V.channels;
   uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
       const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz);
       if (v < (R)0) continue;
       R c[4];
-      tf_eval<R>(V.tf, v, c);
+      tf_eval<R>(V.tf, V.slope, v, c);
       const R w = ((R)1 - A) * c[3];
       C[0] += w * c[0];
       C[1] += w * c[1];
@@ -225,6 +229,243 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
       dst[0] = to_u8_unit<R>(A);
     }
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// fp32 fast path for the extension modes (MIP, alpha): the volume is bound to a
+// layered 2D texture (one layer per z-slice, block-linear, clamp addressing)
+// and every trilinear sample is TWO gathers (tld4: the 2x2 footprint of slice
+// z0 and of slice z1) instead of eight byte loads.  The geometry, sample
+// positions, clamping and skip rule are those of render.py:68-140; the
+// interpolation weights are computed in fp32 (tolerance 1/255).
+__device__ __forceinline__ uint4 tld4_a2d(cudaTextureObject_t tex, int layer, float x, float y) {
+  uint4 r;
+  asm volatile("tld4.r.a2d.v4.u32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(tex), "r"(layer), "f"(x), "f"(y));
+  return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex, int nx, int ny, int nz,
+                                                         const __grid_constant__ ViewBatch views, int dim, int row0,
+                                                         int row1, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = row0 + blockIdx.y;
+  const int view = blockIdx.z;
+  if (i >= dim || j >= row1) return;
+  const ViewDev& V = views.v[view];
+  const RenderGeom& G = V.g;
+  const int ch = V.channels;
+  uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
+  const double wy = G.big_r - ((double)j + 0.5) * G.px_size;
+  const double wx = -G.big_r + ((double)i + 0.5) * G.px_size;
+  const double ox = G.rx * wx, oy = G.ry * wx, oz = wy;
+  const int steps = V.steps;
+  int klo = 0, khi = steps - 1;
+  const double n_max = G.inv_vx;
+  clip_axis(ox, G.dx, (double)nx / (2.0 * n_max), G.big_r, G.dt, steps, klo, khi);
+  clip_axis(oy, G.dy, (double)ny / (2.0 * n_max), G.big_r, G.dt, steps, klo, khi);
+  const double uzd = oz * G.inv_vx + (double)(nz - 1) * 0.5;
+  if (uzd < -0.5 || uzd > (double)nz - 0.5) { klo = steps; khi = -1; }
+  if (klo < 0) klo = 0;
+  if (khi > steps - 1) khi = steps - 1;
+  // per-row constants: the row's two slices and z weight (render.py:72-79, 105-111)
+  const int zf = (int)floor(uzd);
+  const float fz = (float)(uzd - (double)zf);
+  const int l0 = min(max(zf, 0), nz - 1), l1 = min(max(zf + 1, 0), nz - 1);
+  // u(k) = a + k * b exactly as an FMA per step (no drift): u = (o + d*t)*n + (n-1)/2, t = -R + (k+1/2)dt
+  const double bx = G.dx * G.dt * G.inv_vx, by = G.dy * G.dt * G.inv_vx;
+  const double ax = (ox + G.dx * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(nx - 1) * 0.5;
+  const double ay = (oy + G.dy * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(ny - 1) * 0.5;
+  const float fax = (float)ax, fbx = (float)bx, fay = (float)ay, fby = (float)by;
+  const float xlo = -0.5f, xhi = (float)nx - 0.5f, ylo = -0.5f, yhi = (float)ny - 0.5f;
+  float m = 0.f;
+  float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+  const float stop = V.early_stop;
+  for (int k = klo; k <= khi; k++) {
+    const float ux = fmaf((float)k, fbx, fax), uy = fmaf((float)k, fby, fay);
+    if (ux < xlo || ux > xhi || uy < ylo || uy > yhi) continue;
+    const float x0 = floorf(ux), y0 = floorf(uy);
+    const float fx = ux - x0, fy = uy - y0;
+    // tld4 footprint at (x0 + 1, y0 + 1): .w = (x0, y0), .z = (x0+1, y0), .x = (x0, y0+1), .y = (x0+1, y0+1)
+    const uint4 g0 = tld4_a2d(tex, l0, x0 + 1.0f, y0 + 1.0f);
+    const uint4 g1 = tld4_a2d(tex, l1, x0 + 1.0f, y0 + 1.0f);
+    const float a00 = fmaf(fx, (float)g0.z - (float)g0.w, (float)g0.w);
+    const float a10 = fmaf(fx, (float)g0.y - (float)g0.x, (float)g0.x);
+    const float b00 = fmaf(fx, (float)g1.z - (float)g1.w, (float)g1.w);
+    const float b10 = fmaf(fx, (float)g1.y - (float)g1.x, (float)g1.x);
+    const float c0 = fmaf(fy, a10 - a00, a00), c1 = fmaf(fy, b10 - b00, b00);
+    const float v = fmaf(fz, c1 - c0, c0);
+    if (MODE == CTP_MODE_MIP) {
+      m = fmaxf(m, v);
+    } else {
+      float c[4];
+      tf_eval<float>(V.tf, V.slope, v, c);
+      const float w = (1.f - A) * c[3];
+      C0 = fmaf(w, c[0], C0);
+      C1 = fmaf(w, c[1], C1);
+      C2 = fmaf(w, c[2], C2);
+      A += w;
+      if (A >= stop) break;
+    }
+  }
+  if (MODE == CTP_MODE_MIP) {
+    const uint8_t o = (uint8_t)(int)floorf(fminf(m, 255.f) + 0.5f);
+    if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(o, o, o, 255);
+    else dst[0] = o;
+  } else {
+    if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(to_u8_unit<float>(C0), to_u8_unit<float>(C1),
+                                                              to_u8_unit<float>(C2), to_u8_unit<float>(A));
+    else dst[0] = to_u8_unit<float>(A);
+  }
+}
+
+// Row planes: every image row j of the turntable lives at one z (render.py:140),
+// so its two slices can be blended ONCE per volume into an fp32 plane
+//   P_j(x, y) = (1 - fz_j) V[z0_j](x, y) + fz_j V[z0_j + 1](x, y)
+// shared by all azimuths; a trilinear sample is then ONE gather (tld4) +
+// a bilinear blend.  Mathematically the reference's trilinear (z applied last
+// vs first only changes fp rounding, tolerance 1/255).
+__device__ __forceinline__ float4 tld4f_a2d(cudaTextureObject_t tex, int layer, float x, float y) {
+  float4 r;
+  asm volatile("tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(tex), "r"(layer), "f"(x), "f"(y));
+  return r;
+}
+
+__global__ void blend_rows_kernel(const uint8_t* __restrict__ vol, int nx, int ny, int nz, double big_r, double px_size,
+                                  double inv_vx, int row0, cudaSurfaceObject_t surf) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int layer = blockIdx.z;
+  if (x >= nx) return;
+  const int j = row0 + layer;
+  const double wy = big_r - ((double)j + 0.5) * px_size;
+  const double uz = wy * inv_vx + (double)(nz - 1) * 0.5;
+  float v = 0.f;
+  if (!(uz < -0.5 || uz > (double)nz - 0.5)) {
+    const int zf = (int)floor(uz);
+    const float fz = (float)(uz - (double)zf);
+    const int z0 = min(max(zf, 0), nz - 1), z1 = min(max(zf + 1, 0), nz - 1);
+    const float a = (float)__ldg(vol + ((int64_t)z0 * ny + y) * nx + x);
+    const float b = (float)__ldg(vol + ((int64_t)z1 * ny + y) * nx + x);
+    v = fmaf(fz, b - a, a);
+  }
+  // 8.8 fixed point: |error| <= 1/512 of a gray level
+  surf2DLayeredwrite((unsigned short)__float2uint_rn(v * 256.0f), surf, x * (int)sizeof(unsigned short), y, layer);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t tex, int nx, int ny, int nz,
+                                                          const __grid_constant__ ViewBatch views, int dim, int row0,
+                                                          int row1, uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = row0 + blockIdx.y;
+  const int view = blockIdx.z;
+  if (i >= dim || j >= row1) return;
+  const ViewDev& V = views.v[view];
+  const RenderGeom& G = V.g;
+  const int ch = V.channels;
+  uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
+  const double wy = G.big_r - ((double)j + 0.5) * G.px_size;
+  const double wx = -G.big_r + ((double)i + 0.5) * G.px_size;
+  const double ox = G.rx * wx, oy = G.ry * wx, oz = wy;
+  const int steps = V.steps;
+  int klo = 0, khi = steps - 1;
+  const double n_max = G.inv_vx;
+  clip_axis(ox, G.dx, (double)nx / (2.0 * n_max), G.big_r, G.dt, steps, klo, khi);
+  clip_axis(oy, G.dy, (double)ny / (2.0 * n_max), G.big_r, G.dt, steps, klo, khi);
+  const double uzd = oz * G.inv_vx + (double)(nz - 1) * 0.5;
+  if (uzd < -0.5 || uzd > (double)nz - 0.5) { klo = steps; khi = -1; }
+  if (klo < 0) klo = 0;
+  if (khi > steps - 1) khi = steps - 1;
+  const int layer = j - row0;
+  const double bx = G.dx * G.dt * G.inv_vx, by = G.dy * G.dt * G.inv_vx;
+  const double ax = (ox + G.dx * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(nx - 1) * 0.5;
+  const double ay = (oy + G.dy * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(ny - 1) * 0.5;
+  const float fax = (float)ax, fbx = (float)bx, fay = (float)ay, fby = (float)by;
+  const float xlo = -0.5f, xhi = (float)nx - 0.5f, ylo = -0.5f, yhi = (float)ny - 0.5f;
+  float m = 0.f;
+  float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
+  const float stop = V.early_stop;
+#pragma unroll 4
+  for (int k = klo; k <= khi; k++) {
+    const float ux = fmaf((float)k, fbx, fax), uy = fmaf((float)k, fby, fay);
+    if (ux < xlo || ux > xhi || uy < ylo || uy > yhi) continue;
+    const float x0 = floorf(ux), y0 = floorf(uy);
+    const float fx = ux - x0, fy = uy - y0;
+    const uint4 gi = tld4_a2d(tex, layer, x0 + 1.0f, y0 + 1.0f);  // .w (x0,y0) .z (x1,y0) .x (x0,y1) .y (x1,y1)
+    const float4 g = make_float4((float)gi.x, (float)gi.y, (float)gi.z, (float)gi.w);
+    const float a0 = fmaf(fx, g.z - g.w, g.w), a1 = fmaf(fx, g.y - g.x, g.x);
+    const float v = fmaf(fy, a1 - a0, a0) * (1.0f / 256.0f);
+    if (MODE == CTP_MODE_MIP) {
+      m = fmaxf(m, v);
+    } else {
+      float c[4];
+      tf_eval<float>(V.tf, V.slope, v, c);
+      const float w = (1.f - A) * c[3];
+      C0 = fmaf(w, c[0], C0);
+      C1 = fmaf(w, c[1], C1);
+      C2 = fmaf(w, c[2], C2);
+      A += w;
+      if (A >= stop) break;
+    }
+  }
+  if (MODE == CTP_MODE_MIP) {
+    const uint8_t o = (uint8_t)(int)floorf(fminf(m, 255.f) + 0.5f);
+    if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(o, o, o, 255);
+    else dst[0] = o;
+  } else {
+    if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(to_u8_unit<float>(C0), to_u8_unit<float>(C1),
+                                                              to_u8_unit<float>(C2), to_u8_unit<float>(A));
+    else dst[0] = to_u8_unit<float>(A);
+  }
+}
+
+struct RowPlanes {
+  cudaArray_t arr = nullptr;
+  cudaTextureObject_t tex = 0;
+  cudaSurfaceObject_t surf = 0;
+  ~RowPlanes() {
+    if (tex) cudaDestroyTextureObject(tex);
+    if (surf) cudaDestroySurfaceObject(surf);
+    if (arr) cudaFreeArray(arr);
+  }
+};
+
+struct TexVolume {
+  cudaArray_t arr = nullptr;
+  cudaTextureObject_t tex = 0;
+  ~TexVolume() {
+    if (tex) cudaDestroyTextureObject(tex);
+    if (arr) cudaFreeArray(arr);
+  }
+};
+
+static int make_tex_volume(TexVolume& tv, const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, cudaStream_t st) {
+  cudaChannelFormatDesc fd = cudaCreateChannelDesc<unsigned char>();
+  CTP_CUDA_CALL(cudaMalloc3DArray(&tv.arr, &fd, make_cudaExtent((size_t)nx, (size_t)ny, (size_t)nz), cudaArrayLayered));
+  cudaMemcpy3DParms p = {};
+  p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(vol), (size_t)nx, (size_t)nx, (size_t)ny);
+  p.dstArray = tv.arr;
+  p.extent = make_cudaExtent((size_t)nx, (size_t)ny, (size_t)nz);
+  p.kind = cudaMemcpyDeviceToDevice;
+  CTP_CUDA_CALL(cudaMemcpy3DAsync(&p, st));
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = tv.arr;
+  cudaTextureDesc td = {};
+  td.addressMode[0] = cudaAddressModeClamp;
+  td.addressMode[1] = cudaAddressModeClamp;
+  td.addressMode[2] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  CTP_CUDA_CALL(cudaCreateTextureObject(&tv.tex, &rd, &td, nullptr));
+  return CTP_OK;
 }
 
 __global__ void image_hist_kernel(const uint8_t* __restrict__ imgs, int64_t pixels, unsigned long long* __restrict__ hist) {
@@ -258,8 +499,8 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const 
   CTP_REQUIRE(dim >= 16, CTP_E_INVALID, "image_dim %d below minimum 16", dim);
   CTP_REQUIRE(0 <= row0 && row0 < row1 && row1 <= dim, CTP_E_INVALID, "rows [%lld, %lld) outside [0, %d]",
               (long long)row0, (long long)row1, dim);
-  ViewDev hv[64];
-  CTP_REQUIRE(n_views <= 64, CTP_E_INVALID, "at most 64 views per call (got %d)", n_views);
+  ViewDev hv[kMaxViews];
+  CTP_REQUIRE(n_views <= kMaxViews, CTP_E_INVALID, "at most %d views per call (got %d)", kMaxViews, n_views);
   const int64_t n_max = nx > ny ? (nx > nz ? nx : nz) : (ny > nz ? ny : nz);
   for (int q = 0; q < n_views; q++) {
     const ctp_view& v = views[q];
@@ -290,21 +531,77 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const 
     hv[q].gain = v.gain;
     for (int a = 0; a < 4; a++)
       for (int b = 0; b < 5; b++) hv[q].tf[a][b] = v.tf[a][b];
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 4; b++) {
+        const double c0 = v.tf[a][b + 1], c1 = v.tf[a + 1][b + 1], x0 = v.tf[a][0], x1 = v.tf[a + 1][0];
+        // fp64 views: the slope in double (as the oracle); fp32 views: in float, as it would be per sample
+        hv[q].slope[a][b] = v.fp32 ? (double)(((float)c1 - (float)c0) / ((float)x1 - (float)x0)) : (c1 - c0) / (x1 - x0);
+      }
     hv[q].early_stop = v.early_stop;
   }
   cudaStream_t st = as_stream(stream);
-  ViewDev* dv = nullptr;
-  CTP_CUDA_CALL(cudaMallocAsync(reinterpret_cast<void**>(&dv), sizeof(ViewDev) * n_views, st));
-  CTP_CUDA_CALL(cudaMemcpyAsync(dv, hv, sizeof(ViewDev) * n_views, cudaMemcpyHostToDevice, st));
+  ViewBatch vb;
+  for (int q = 0; q < n_views; q++) vb.v[q] = hv[q];
   dim3 grid((dim + 127) / 128, (unsigned)(row1 - row0), (unsigned)n_views);
+  const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && nz <= 2048 &&
+                        nx <= 32768 && ny <= 32768;
+  if (tex_path) {
+    // row planes when they fit comfortably (4 B per voxel per image row)
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t plane_bytes = (size_t)(row1 - row0) * (size_t)nx * (size_t)ny * 2;
+    const char* rp_env = getenv("CTP_RENDER_ROWPLANES");  // "0" forces the two-gather path
+    if (!(rp_env && rp_env[0] == '0') && row1 - row0 <= 2048 && plane_bytes < free_b / 2) {
+      RowPlanes rp;
+      cudaChannelFormatDesc fd = cudaCreateChannelDesc<unsigned short>();
+      CTP_CUDA_CALL(cudaMalloc3DArray(&rp.arr, &fd, make_cudaExtent((size_t)nx, (size_t)ny, (size_t)(row1 - row0)),
+                                      cudaArrayLayered | cudaArraySurfaceLoadStore));
+      cudaResourceDesc rd = {};
+      rd.resType = cudaResourceTypeArray;
+      rd.res.array.array = rp.arr;
+      CTP_CUDA_CALL(cudaCreateSurfaceObject(&rp.surf, &rd));
+      cudaTextureDesc td = {};
+      td.addressMode[0] = cudaAddressModeClamp;
+      td.addressMode[1] = cudaAddressModeClamp;
+      td.addressMode[2] = cudaAddressModeClamp;
+      td.filterMode = cudaFilterModePoint;
+      td.readMode = cudaReadModeElementType;
+      td.normalizedCoords = 0;
+      CTP_CUDA_CALL(cudaCreateTextureObject(&rp.tex, &rd, &td, nullptr));
+      const RenderGeom& G0 = hv[0].g;
+      dim3 bg((unsigned)((nx + 127) / 128), (unsigned)ny, (unsigned)(row1 - row0));
+      blend_rows_kernel<<<bg, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx, (int)row0,
+                                            rp.surf);
+      CTP_CUDA_CHECK_LAUNCH("blend_rows_kernel");
+      if (v0.mode == CTP_MODE_MIP)
+        render_rows_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                               (int)row1, out);
+      else
+        render_rows_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                                 (int)row1, out);
+      CTP_CUDA_CHECK_LAUNCH("render_rows_kernel");
+      CTP_CUDA_CALL(cudaStreamSynchronize(st));  // planes must outlive the kernel
+      return CTP_OK;
+    }
+    TexVolume tv;
+    int rc = make_tex_volume(tv, vol, nz, ny, nx, st);
+    if (rc != CTP_OK) return rc;
+    if (v0.mode == CTP_MODE_MIP)
+      render_tex_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(tv.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                            (int)row1, out);
+    else
+      render_tex_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(tv.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                              (int)row1, out);
+    CTP_CUDA_CHECK_LAUNCH("render_tex_kernel");
+    // the array / texture object must outlive the kernel
+    CTP_CUDA_CALL(cudaStreamSynchronize(st));
+    return CTP_OK;
+  }
   if (v0.fp32)
-    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, dv, dim, (int)row0, (int)row1, out);
+    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
   else
-    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, dv, dim, (int)row0, (int)row1, out);
-  cudaError_t le = cudaGetLastError();
-  cudaFreeAsync(dv, st);
-  CTP_REQUIRE(le == cudaSuccess, CTP_E_CUDA, "render_kernel: %s", cudaGetErrorString(le));
-  ++launch_counter();
+    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
+  CTP_CUDA_CHECK_LAUNCH("render_kernel");
   return CTP_OK;
 }
 
