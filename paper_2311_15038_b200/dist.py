@@ -104,7 +104,11 @@ class ShardedPreview:
     group: object = None
 
     def __post_init__(self):
+        self.fused_events = None  # optional (start, end) CUDA events around the fused pass (bench)
         nz, ny, nx = self.shape
+        for s, l in self.level_of.items():  # scheme s must be exactly level l (pipeline.py:221-222)
+            if (nx >> l, ny >> l, nz >> l) != (min(s, nx), min(s, ny), min(s, nz)) or (nx | ny | nz) % (1 << l):
+                raise ValueError(f"scheme {s} is not the power-of-two level {l} of {self.shape}")
         self.align = slab_alignment(self.schemes, self.level_of)
         self.z0, self.z1 = slab_bounds(nz, self.world, self.rank, self.align)
         last0, last1 = slab_bounds(nz, self.world, self.world - 1, self.align)
@@ -132,7 +136,11 @@ class ShardedPreview:
         if self.world > 1:
             dist.broadcast(lut, src=owner, group=self.group)
         self.hist.zero_()
+        if self.fused_events is not None:
+            self.fused_events[0].record()
         self.compute.fused(slab, lut, self.z0, nz, self.hist, self.atlases)
+        if self.fused_events is not None:
+            self.fused_events[1].record()
         if self.world > 1:
             dist.all_reduce(self.hist, group=self.group)
             if gather:
