@@ -250,3 +250,53 @@ def test_batched_views_equal_single_views(P, golden):
     batch = P.render_views(vol, ps)
     for k, p in enumerate(ps):
         assert np.array_equal(batch[k], O.render_view(golden["lphantom"], p.azimuth_deg, 48, 64, "surface", 60))
+
+
+# ---------------------------------------------------------------- config 3 at full size (16 GiB)
+
+def test_preview_c3_full_size_spot_checks(P, cuda):
+    """Config 3 exactly (2048^3 12-bit u16, 20 shells, speckle): the 4096-bin
+    histogram is checked against per-slab oracle bincounts (exact, chunked), the
+    artifact LUT against the oracle on the top slab, and every level's atlas at
+    2000 random cells against the block mean recomputed from the source voxels
+    (a size-independent property: the oracle never holds the 16 GiB volume)."""
+    import torch
+    from paper_2311_15038_b200 import device as dev, synth
+    from paper_2311_15038_b200.device import AtlasSpec
+    from paper_2311_15038_b200.pipeline import plan_preview, run_preview
+
+    spec = synth.config("c3")
+    vol = synth.generate(spec, device=cuda)
+    nz, ny, nx = spec.shape
+    schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec(512, 4096, 8, 8),
+               256: AtlasSpec(256, 2048, 8, 4), 128: AtlasSpec(128, 1024, 8, 2)}
+    plan = plan_preview(spec.shape, schemes)
+    assert not plan.general and plan.nlev == 4
+    res = run_preview(vol, plan)
+    hist = res.hist.cpu().numpy()
+    # exact histogram, 128-slice slabs on the host
+    want = np.zeros(4096, dtype=np.int64)
+    for z in range(0, nz, 128):
+        want += O.histogram_u16(vol[z:z + 128].cpu().numpy())
+    assert np.array_equal(hist, want)
+    top = vol[nz - 3:].cpu().numpy()
+    bins = O.artifact_bins_u16(top)
+    lut = O.lut_u16(bins)
+    assert np.array_equal(res.lut.cpu().numpy(), lut)
+    rng = np.random.default_rng(3)
+    for s, l in plan.scheme_level.items():
+        sp = schemes[s]
+        atl = res.atlases[s]
+        b = 1 << l
+        for _ in range(2000 // 4):
+            kz, y, x = (int(rng.integers(0, nz >> l)), int(rng.integers(0, ny >> l)), int(rng.integers(0, nx >> l)))
+            blk = vol[kz * b:(kz + 1) * b, y * b:(y + 1) * b, x * b:(x + 1) * b].cpu().numpy()
+            f = lut[np.minimum(blk, 4095)].astype(np.int64)
+            cnt = b ** 3
+            expect = (2 * int(f.sum()) + cnt) // (2 * cnt)          # volume.py:306-308
+            m, w = divmod(kz, sp.grid * sp.grid)
+            cy, cx = divmod(w, sp.grid)
+            got = int(atl[m, cy * sp.s + y, cx * sp.s + x].item())
+            assert got == expect, (s, kz, y, x)
+    del vol
+    torch.cuda.empty_cache()

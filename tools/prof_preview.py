@@ -28,7 +28,12 @@ vol = synth.generate(spec)
 schemes = {}
 for s in a.schemes.split(","):
     s = int(s)
-    schemes[s] = AtlasSpec.of(plan_scheme(s)) if s in (128, 256, 512) else AtlasSpec(s, 8 * s, 8, -(-s // 64))
+    if s in (128, 256, 512):
+        schemes[s] = AtlasSpec.of(plan_scheme(s))
+    elif s == 1024:  # config 3 level 1: 64 maps of 4x4 slices, capped at 4096^2
+        schemes[s] = AtlasSpec(1024, 4096, 4, 64)
+    else:
+        schemes[s] = AtlasSpec(s, 8 * s, 8, -(-s // 64))
 plan = plan_preview(spec.shape, schemes)
 lut, _ = dev.artifact_lut(vol)
 hist = torch.zeros(256 if spec.dtype == "u8" else 4096, dtype=torch.int64, device="cuda")
@@ -45,6 +50,7 @@ for _ in range(a.reps):
     ts.append(e0.elapsed_time(e1))
 if a.time:
     alg = vol.numel() * vol.element_size() + sum(t.numel() for t in outs.values())
+    print(f"voxels={vol.numel()} alg_bytes={alg} GVoxel/s={vol.numel() / min(ts) / 1e6:.1f}")
     best = min(ts)
     print(f"variant={os.environ.get('CTP_PREVIEW_VARIANT', 'default')} config={a.config} best_ms={best:.4f} "
           f"median_ms={sorted(ts)[len(ts) // 2]:.4f} GB/s={alg / best / 1e6:.1f}")
