@@ -567,9 +567,15 @@ static int preview_variant() {
 
 template <typename T, int L>
 static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
+  // defaults measured on B200 (tools/prof_preview.py): u8 is bound by the
+  // shared-memory atomic pipe and gains from 32 warps/SM; u16 prefers 16
   switch (preview_variant()) {
+    case 1: return launch_v<T, L, 512, 2, 1024>(a, vol, st);
     case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
-    default: return launch_v<T, L, 512, 2, 1024>(a, vol, st);
+    case 3: return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
+    default:
+      if constexpr (sizeof(T) == 1) return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
+      else return launch_v<T, L, 512, 2, 1024>(a, vol, st);
   }
 }
 
