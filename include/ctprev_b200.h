@@ -88,6 +88,18 @@ int ctp_hist_u16(const uint16_t* vol, int64_t nz, int64_t ny, int64_t nx,
 int ctp_lut_build(const uint64_t* top_hist, int32_t nbins, uint64_t cutoff_floor,
                   int32_t rescale_vmax, uint8_t* lut, uint8_t* flags, void* stream);
 
+/* The whole artifact-LUT step in ONE launch (mask.py:215-231 + 241-245): the
+ * histogram of the top n_top slices of vol (elem_bytes 1: 256 bins, identity
+ * LUT, rescale_vmax 0; elem_bytes 2: 4096 bins, filter o rescale), the LUT and
+ * flags as ctp_lut_build, and -- if zero_hist != NULL -- zeroing of the
+ * nbins-entry histogram the following fused pass accumulates into.
+ * workspace: uint64[4097] that is ZERO on entry and left zero on return (the
+ * last CTA resets it), so one zero-initialised buffer serves every call on
+ * one stream. */
+int ctp_artifact_lut(const void* vol, int32_t elem_bytes, int64_t nz, int64_t ny, int64_t nx, int32_t n_top,
+                     uint64_t cutoff_floor, int32_t rescale_vmax, uint8_t* lut, uint8_t* flags, uint64_t* zero_hist,
+                     uint64_t* workspace, void* stream);
+
 /* Replaces mask.py:246 lut[volume.voxels] (filter_histogram_bins), for any
  * layout/size: out[i] = lut[in[i]] over n bytes.  If hist != NULL the raw
  * input histogram (256 bins) is accumulated in the same pass. */

@@ -189,6 +189,77 @@ __global__ void lut_apply_tail_kernel(const uint8_t* __restrict__ in, uint8_t* _
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// One launch for the whole artifact-LUT step (mask.py:215-231 + 241-245):
+// every CTA histograms a share of the top slab in shared memory and adds it to
+// a global workspace; the LAST CTA to finish (grid-wide counter) builds the
+// LUT and flags, zeroes the caller's main histogram for the coming fused pass,
+// and resets the workspace, which therefore stays zero between calls.
+template <typename T>
+__global__ void __launch_bounds__(256) artifact_lut_kernel(const T* __restrict__ p, int64_t n, int nbins,
+                                                           unsigned long long cutoff_floor, int vmax,
+                                                           uint8_t* __restrict__ lut, uint8_t* __restrict__ flags,
+                                                           unsigned long long* __restrict__ zero_hist,
+                                                           unsigned long long* __restrict__ ws) {
+  __shared__ uint32_t hs[4096];  // u8: 8 warp-private copies of 256 bins (merged below)
+  __shared__ bool last;
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) hs[i] = 0;
+  __syncthreads();
+  const uint32_t top = (uint32_t)nbins - 1;
+  constexpr int PER = 16 / sizeof(T);  // elements per 16-byte vector
+  const int64_t nv = (reinterpret_cast<uintptr_t>(p) & 15) == 0 ? n / PER : 0;  // scalar if unaligned
+  const uint4* pv = reinterpret_cast<const uint4*>(p);
+  uint32_t* wh = hs + (sizeof(T) == 1 ? (threadIdx.x >> 5) * 256 : 0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 q = __ldg(pv + i);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if constexpr (sizeof(T) == 1) {
+#pragma unroll
+        for (int b = 0; b < 4; b++) atomicAdd(&wh[(w[k] >> (8 * b)) & 255u], 1u);
+      } else {
+        atomicAdd(&wh[min(w[k] & 0xFFFFu, top)], 1u);
+        atomicAdd(&wh[min(w[k] >> 16, top)], 1u);
+      }
+    }
+  }
+  for (int64_t i = nv * PER + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&wh[min((uint32_t)__ldg(p + i), top)], 1u);
+  __syncthreads();
+  if constexpr (sizeof(T) == 1) {  // merge the warp copies into copy 0
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+      uint32_t t = 0;
+      for (int c = 0; c < (int)(blockDim.x >> 5); c++) t += hs[c * 256 + b];
+      hs[b] = t;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (hs[b]) atomicAdd(ws + b, (unsigned long long)hs[b]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ws + 4096, 1ull) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+    const unsigned long long c = atomicExch(ws + b, 0ull);  // read + reset
+    const bool flagged = (b == 0) || (c > cutoff_floor);     // mask.py:230-231
+    uint32_t val = (uint32_t)b;
+    if (vmax > 0) {
+      const uint32_t v = min((uint32_t)b, (uint32_t)vmax);
+      val = (uint32_t)((2ull * 255ull * v + (uint64_t)vmax) / (2ull * (uint64_t)vmax));
+    }
+    lut[b] = flagged ? 0 : (uint8_t)val;
+    if (flags) flags[b] = flagged ? 1 : 0;
+  }
+  if (zero_hist)
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) zero_hist[b] = 0;
+  if (threadIdx.x == 0) ws[4096] = 0;
+}
+
 static int grid_for(int64_t work_items, int per_block, int blocks_per_sm) {
   int64_t g = (work_items + per_block - 1) / per_block;
   const int64_t cap = (int64_t)num_sms() * blocks_per_sm;
@@ -244,6 +315,33 @@ int ctp_lut_build(const uint64_t* top_hist, int32_t nbins, uint64_t cutoff_floor
   lut_build_kernel<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(top_hist), nbins,
                                                       (unsigned long long)cutoff_floor, rescale_vmax, lut, flags);
   CTP_CUDA_CHECK_LAUNCH("lut_build_kernel");
+  return CTP_OK;
+}
+
+int ctp_artifact_lut(const void* vol, int32_t elem_bytes, int64_t nz, int64_t ny, int64_t nx, int32_t n_top,
+                     uint64_t cutoff_floor, int32_t rescale_vmax, uint8_t* lut, uint8_t* flags, uint64_t* zero_hist,
+                     uint64_t* workspace, void* stream) {
+  CTP_REQUIRE(vol && lut && workspace, CTP_E_INVALID, "ctp_artifact_lut: null pointer");
+  CTP_REQUIRE(elem_bytes == 1 || elem_bytes == 2, CTP_E_UNSUPPORTED, "elem_bytes must be 1 or 2");
+  CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1, CTP_E_INVALID, "ctp_artifact_lut: degenerate shape");
+  CTP_REQUIRE(1 <= n_top && n_top <= nz, CTP_E_INVALID, "n_top %d outside [1, %lld]", n_top, (long long)nz);  // mask.py:223-224
+  CTP_REQUIRE(rescale_vmax >= 0 && (elem_bytes == 2) == (rescale_vmax > 0), CTP_E_INVALID,
+              "u8 takes the identity LUT (vmax 0), u16 the 16->8 rescale (vmax > 0)");
+  const int nbins = elem_bytes == 1 ? 256 : 4096;
+  const int64_t slice = ny * nx;
+  const int64_t n = (int64_t)n_top * slice;
+  const int grid = grid_for(n / (16 / elem_bytes), 256 * 4, 2);
+  auto* h = reinterpret_cast<unsigned long long*>(zero_hist);
+  auto* w = reinterpret_cast<unsigned long long*>(workspace);
+  if (elem_bytes == 1)
+    artifact_lut_kernel<uint8_t><<<grid, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint8_t*>(vol) + (nz - n_top) * slice, n, nbins, (unsigned long long)cutoff_floor, 0, lut,
+        flags, h, w);
+  else
+    artifact_lut_kernel<uint16_t><<<grid, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint16_t*>(vol) + (nz - n_top) * slice, n, nbins, (unsigned long long)cutoff_floor,
+        rescale_vmax, lut, flags, h, w);
+  CTP_CUDA_CHECK_LAUNCH("artifact_lut_kernel");
   return CTP_OK;
 }
 

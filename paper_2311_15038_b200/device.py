@@ -95,6 +95,38 @@ def artifact_lut(vol: torch.Tensor, n_top: int = 3, frac: float = 0.0005):
     return lut_from_hist(th, top_size, frac, VMAX_U16)
 
 
+_WORKSPACES: dict = {}
+
+
+def _workspace(device) -> torch.Tensor:
+    """Zero-initialised uint64[4097] per (device, stream) for ctp_artifact_lut (kept zero by the kernel)."""
+    key = (device.index if isinstance(device, torch.device) else device, torch.cuda.current_stream().cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = torch.zeros(4097, dtype=torch.int64, device=device)
+        _WORKSPACES[key] = ws
+    return ws
+
+
+def artifact_lut_fused(vol: torch.Tensor, n_top: int = 3, frac: float = 0.0005,
+                       zero_hist: torch.Tensor | None = None, lut: torch.Tensor | None = None,
+                       flags: torch.Tensor | None = None):
+    """The artifact-LUT step in ONE launch (top-slab histogram + LUT + flags), also
+    zeroing ``zero_hist`` for the fused pass that follows."""
+    is16 = vol.dtype == torch.uint16
+    _check_dev(vol, torch.uint16 if is16 else torch.uint8, "artifact_lut_fused")
+    nz, ny, nx = vol.shape
+    nbins = NBINS_U16 if is16 else NBINS_U8
+    if lut is None:
+        lut = torch.empty(nbins, dtype=torch.uint8, device=vol.device)
+    if flags is None:
+        flags = torch.empty(nbins, dtype=torch.uint8, device=vol.device)
+    _lib.call("ctp_artifact_lut", _ptr(vol), 2 if is16 else 1, nz, ny, nx, n_top,
+              cutoff_floor(frac, n_top * ny * nx), VMAX_U16 if is16 else 0, _ptr(lut), _ptr(flags), _ptr(zero_hist),
+              _ptr(_workspace(vol.device)), _stream())
+    return lut, flags
+
+
 def lut_apply_u8(src: torch.Tensor, lut: torch.Tensor | None, out: torch.Tensor | None = None,
                  hist: torch.Tensor | None = None) -> torch.Tensor:
     """mask.py:246 on the device (any shape); optionally accumulates the raw histogram."""

@@ -80,8 +80,11 @@ class DeviceSlabCompute(SlabCompute):
         self.nbins = dev.NBINS_U8 if dtype == torch.uint8 else dev.NBINS_U16
         self.fused_levels = fused_levels  # level -> AtlasSpec
 
-    def artifact_lut(self, top_slab, n_top, frac):
-        return self.dev.artifact_lut(top_slab, n_top, frac)[0]
+    def artifact_lut(self, top_slab, n_top, frac, zero_hist=None):
+        # one launch: top-slab histogram + LUT (+ zeroing the step's histogram)
+        self._lut, _ = self.dev.artifact_lut_fused(top_slab, n_top, frac, zero_hist=zero_hist,
+                                                   lut=getattr(self, "_lut", None))
+        return self._lut
 
     def fused(self, slab, lut, z_base, full_nz, hist, atlases):
         self.dev.preview(slab, lut, self.fused_levels, hist=hist, z_base=z_base, full_nz=full_nz,
@@ -129,13 +132,20 @@ class ShardedPreview:
         """slab: this rank's [z0, z1) voxels on ``device``.  Returns {hist, lut, atlases} (complete on rank 0)."""
         nz = self.shape[0]
         owner = self.world - 1
+        zeroed = False
         if self.rank == owner:
-            lut = self.compute.artifact_lut(slab[slab.shape[0] - self.n_top:], self.n_top, self.frac)
+            top = slab[slab.shape[0] - self.n_top:]
+            if isinstance(self.compute, DeviceSlabCompute):
+                lut = self.compute.artifact_lut(top, self.n_top, self.frac, zero_hist=self.hist)
+                zeroed = True
+            else:
+                lut = self.compute.artifact_lut(top, self.n_top, self.frac)
         else:
             lut = torch.empty(self.compute.nbins, dtype=torch.uint8, device=self.device)
         if self.world > 1:
             dist.broadcast(lut, src=owner, group=self.group)
-        self.hist.zero_()
+        if not zeroed:
+            self.hist.zero_()
         if self.fused_events is not None:
             self.fused_events[0].record()
         self.compute.fused(slab, lut, self.z0, nz, self.hist, self.atlases)

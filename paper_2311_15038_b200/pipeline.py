@@ -92,16 +92,22 @@ def run_preview(vol: torch.Tensor, plan: PreviewPlan, n_top: int = 3, frac: floa
                 hist: torch.Tensor | None = None) -> DevicePreview:
     """All device work for one volume on the current stream (no sync)."""
     nbins = dev.NBINS_U8 if vol.dtype == torch.uint8 else dev.NBINS_U16
-    lut, flags = dev.artifact_lut(vol, n_top, frac)
-    if hist is None:
-        hist = torch.zeros(nbins, dtype=torch.int64, device=vol.device)
-    outs = dev.preview(vol, lut, plan.fused, hist=hist)
+    if hist is None:  # one launch: top-slab histogram + LUT + zeroing of the histogram
+        hist = torch.empty(nbins, dtype=torch.int64, device=vol.device)
+        lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
+    else:
+        lut, flags = dev.artifact_lut_fused(vol, n_top, frac)
+    nz, ny, nx = vol.shape
+    if vol.dtype == torch.uint8 and nx % 16 and set(plan.fused) == {0}:
+        # rows not 16-byte vectorisable: filter + histogram with the any-size LUT kernel
+        outs = {0: dev.lut_apply_u8(vol, lut, hist=hist)}
+    else:
+        outs = dev.preview(vol, lut, plan.fused, hist=hist)
     atlases, levels = {}, {}
     filtered = outs.get(0) if plan.fused.get(0) == "xyz" else None
     for s, l in plan.scheme_level.items():
         if l is not None:
             atlases[s] = outs[l]
-    nz, ny, nx = vol.shape
     for s in plan.general:
         spec = plan.schemes[s]
         lv = dev.downscale(filtered, (min(s, nx), min(s, ny), min(s, nz)))
@@ -179,8 +185,7 @@ class PreviewSession:
             top_ready.record(self.s_h2d)
         with torch.cuda.stream(self.s_cmp):
             self.s_cmp.wait_event(top_ready)
-            self.hist.zero_()
-            lut, flags = dev.artifact_lut(self.top, self.n_top, self.frac)
+            lut, flags = dev.artifact_lut_fused(self.top, self.n_top, self.frac, zero_hist=self.hist)
         n_chunks = (nz + self.chunk - 1) // self.chunk
         free = [None] * len(self.ring)
         for c in range(n_chunks):

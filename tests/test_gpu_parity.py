@@ -300,3 +300,42 @@ def test_preview_c3_full_size_spot_checks(P, cuda):
             assert got == expect, (s, kz, y, x)
     del vol
     torch.cuda.empty_cache()
+
+
+def test_artifact_lut_single_launch(P, cuda):
+    """ctp_artifact_lut == ctp_hist + ctp_lut_build, and leaves its workspace zero
+    (repeated calls, u8 and u16, several n_top / frac)."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(12)
+    v8 = np.clip(np.rint(rng.normal(20, 6, (12, 96, 80))), 0, 255).astype(np.uint8)
+    v8[-2:, :10, :10] = 200
+    v16 = np.clip(np.rint(rng.normal(400, 120, (10, 64, 64))), 0, 4095).astype(np.uint16)
+    for vox, n_tops in ((v8, (1, 3, 12)), (v16, (1, 3))):
+        t = torch.from_numpy(vox).to(cuda)
+        for n_top in n_tops:
+            for frac in (0.0005, 0.0, 0.01):
+                hist = torch.full((256 if vox.dtype == np.uint8 else 4096,), 7, dtype=torch.int64, device=cuda)
+                lut, flags = dev.artifact_lut_fused(t, n_top, frac, zero_hist=hist)
+                if vox.dtype == np.uint8:
+                    bins = O.artifact_bins(vox, n_top, frac)
+                    want = O.filter_lut(bins)
+                else:
+                    bins = O.artifact_bins_u16(vox, n_top, frac)
+                    want = O.lut_u16(bins)
+                assert np.array_equal(lut.cpu().numpy(), want)
+                assert set(np.nonzero(flags.cpu().numpy())[0].tolist()) == set(bins)
+                assert int(hist.abs().sum().item()) == 0
+    for ws in dev._WORKSPACES.values():
+        assert int(ws.abs().sum().item()) == 0
+
+
+def test_artifact_lut_unaligned_top_slab(P, cuda):
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(13)
+    vox = rng.integers(0, 6, size=(5, 7, 11), dtype=np.uint8)   # 77-byte slices: unaligned top slab
+    lut, _ = dev.artifact_lut_fused(torch.from_numpy(vox).to(cuda), 3, 0.01)
+    assert np.array_equal(lut.cpu().numpy(), O.filter_lut(O.artifact_bins(vox, 3, 0.01)))
+    res = P.preview_pipeline(vox, schemes=[P.SlicemapScheme(8, 32, 4, 1)])
+    hist, bins, _, _, atl = O.preview_pipeline(vox, [8], schemes=[(8, 32, 4, 1)])
+    assert np.array_equal(res.histogram, hist) and res.bins == bins
+    assert np.array_equal(np.stack(res.slicemaps[8].atlases), np.stack(atl[0]))
