@@ -25,6 +25,7 @@ BINDINGS = {
     "render_view": ["render", "cli", ""],
     "image_entropy": ["render", "cli", ""],
     "optimal_snapshot": ["render", "pipeline", "cli", ""],
+    "build_data_preview": ["pipeline", ""],
 }
 
 _saved: dict = {}
@@ -43,6 +44,7 @@ def install(package: str = "ctprev") -> list[str]:
     FACTORY.SlicemapSet = sm.SlicemapSet
     FACTORY.EntropyResult = rd.EntropyResult
     FACTORY.SnapshotResult = rd.SnapshotResult
+    FACTORY.DataPreview = importlib.import_module(f"{package}.pipeline").DataPreview
     patched = []
     for name, mods in BINDINGS.items():
         new = getattr(ops, name)

@@ -31,12 +31,12 @@ from . import device as dev
 from .device import AtlasSpec
 from .errors import InvalidTarget, RangeOutOfBounds, UnsupportedPixelFormat, DimensionMismatch
 from .pipeline import plan_preview, run_preview
-from .types import FACTORY, ViewParams, plan_scheme
+from .types import FACTORY, STAGES_DATA, ViewParams, plan_scheme
 
 __all__ = [
     "volume_histogram", "histogram_of", "artifact_bins", "filter_histogram_bins", "downscale_volume",
     "encode_slicemaps", "decode_slicemaps", "render_view", "render_views", "image_entropy",
-    "optimal_snapshot", "preview_pipeline", "PreviewResult", "to_device", "cuda_device",
+    "optimal_snapshot", "preview_pipeline", "PreviewResult", "build_data_preview", "to_device", "cuda_device",
 ]
 
 
@@ -290,3 +290,36 @@ def preview_pipeline(volume, schemes=(512, 256, 128), n_top: int = 3, frac: floa
     filtered = FACTORY.Volume(_host(res.filtered)) if (keep_filtered and res.filtered is not None) else None
     return PreviewResult(_host(res.hist), frozenset(int(b) for b in np.nonzero(flags)[0]), slicemaps, levels,
                          filtered)
+
+
+# ---------------------------------------------------------------------------
+# preview builders
+
+DATA_SCHEME = 256  # pipeline.py:87
+
+
+def build_data_preview(volume):
+    """pipeline.py:240-257 on the device: the 256-scheme level (_scheme_volume,
+    direct from full resolution), its zero-padded atlases, artifact bins from the
+    level's top slices, and the filter.  decode -> filter -> encode of the
+    reference equals the LUT applied to the atlas bytes themselves (the padding
+    is 0 and LUT(0) = 0), so the filter is ONE lut_apply pass over 16 MB."""
+    vox = _voxels(volume)
+    nz, ny, nx = vox.shape
+    s = DATA_SCHEME
+    scheme = plan_scheme(s)
+    spec = AtlasSpec.of(scheme)
+    t = to_device(vox)
+    target = (min(s, nx), min(s, ny), min(s, nz))                     # pipeline.py:221-222
+    down = t if target == (nx, ny, nz) else _downscale_dev(t, target)
+    atl = dev.encode_atlas(down, spec)                                # pipeline.py:249 (+ _pad_to_cube)
+    n_top = 3
+    dz = down.shape[0]
+    if not 1 <= n_top <= dz:                                          # mask.py:223-224
+        raise RangeOutOfBounds(f"n_top {n_top} outside [1, {dz}]")
+    lut, flags = dev.artifact_lut(down, n_top, 0.0005)                # pipeline.py:250
+    fatl = dev.lut_apply_u8(atl, lut)                                 # pipeline.py:251-252
+    a = _host(fatl)
+    bins = tuple(int(b) for b in np.nonzero(_host(flags))[0])
+    sset = FACTORY.SlicemapSet(scheme=scheme, atlases=tuple(a[m] for m in range(spec.map_count)))
+    return FACTORY.DataPreview(slicemaps=sset, filtered_bins=bins, stages=STAGES_DATA)

@@ -225,6 +225,18 @@ class SnapshotResult:
     per_view: tuple
 
 
+STAGES_DATA = ("slicemaps_conversion", "histogram_filtering")  # pipeline.py:82
+
+
+@dataclass(frozen=True)
+class DataPreview:
+    """pipeline.py:116-122."""
+
+    slicemaps: SlicemapSet
+    filtered_bins: tuple
+    stages: tuple
+
+
 class _Factory:
     """Where result objects come from (switched by ``install()``)."""
 
@@ -238,6 +250,7 @@ class _Factory:
         self.SlicemapSet = SlicemapSet
         self.EntropyResult = EntropyResult
         self.SnapshotResult = SnapshotResult
+        self.DataPreview = DataPreview
 
 
 FACTORY = _Factory()

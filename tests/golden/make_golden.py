@@ -5,7 +5,7 @@ Run in the builder container, where /root/reference exists:
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
         python tests/golden/make_golden.py
 
-Writes tests/golden/ref_golden.npz (committed).  The GPU box never reads
+Writes tests/golden/ref_golden.npz and ref_golden_datapreview.npz (committed).  The GPU box never reads
 /root/reference: tests compare the CPU oracle and the CUDA path against these
 frozen reference outputs.
 """
@@ -138,5 +138,47 @@ def main() -> None:
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB, {len(g)} arrays)")
 
 
+
+
+
+def data_preview_golden() -> None:
+    """Reference build_data_preview (pipeline.py:240-257) on two mounted phantoms."""
+    from ctprev.pipeline import build_data_preview
+    out = Path(__file__).resolve().parent / "ref_golden_datapreview.npz"
+    g = {}
+    specs = [
+        PhantomSpec(dims=(160, 160, 96),
+                    container=CylinderSpec(cx=81.0, cy=78.0, r=65.0, wall=2.0, value=(140, 145)),
+                    objects=(SphereSpec(cx=75.0, cy=85.0, cz=40.0, r=22.0, value=(200, 210)),), seed=5),
+        PhantomSpec(dims=(272, 264, 260),
+                    container=CylinderSpec(cx=135.0, cy=131.0, r=120.0, wall=4.0, value=(40, 60)),
+                    objects=(SphereSpec(cx=120.0, cy=140.0, cz=150.0, r=50.0, value=(120, 200)),
+                             BoxSpec((60, 60, 20), (200, 90, 80), value=(90, 95))), seed=9),
+    ]
+    for i, spec in enumerate(specs):
+        vol = generate_phantom(spec).volume
+        dp = build_data_preview(vol)
+        g[f"dp{i}_in"] = vol.voxels.copy()
+        g[f"dp{i}_bins"] = np.array(dp.filtered_bins, dtype=np.int64)
+        g[f"dp{i}_atlases"] = np.stack(dp.slicemaps.atlases)
+    g["dp_n"] = np.array(len(specs))
+    # acceptance criterion 8 (test_acceptance.py:217-244): 36 views, 256^2, 256 steps, surface T=60
+    l_ph = generate_phantom(PhantomSpec(
+        dims=(96, 96, 96),
+        objects=(BoxSpec((8, 40, 8), (88, 56, 24), value=(150, 150)),
+                 BoxSpec((8, 40, 24), (24, 56, 88), value=(220, 220)),
+                 SphereSpec(70.0, 48.0, 60.0, r=10.0, value=(90, 90))),
+        seed=4)).volume
+    snap = optimal_snapshot(l_ph, n_views=36, params=ViewParams(image_dim=256, steps=256, mode=SURFACE, threshold=60))
+    g["acc_snap_az"] = np.array(snap.azimuth_deg)
+    g["acc_snap_h"] = np.array(snap.entropy)
+    g["acc_snap_per_view"] = np.array(snap.per_view, dtype=np.float64)
+    g["acc_snap_img"] = snap.image
+    np.savez_compressed(out, **g)
+    print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
+
+
 if __name__ == "__main__":
-    main()
+    if "--only-extra" not in sys.argv:
+        main()
+    data_preview_golden()

@@ -339,3 +339,31 @@ def test_artifact_lut_unaligned_top_slab(P, cuda):
     hist, bins, _, _, atl = O.preview_pipeline(vox, [8], schemes=[(8, 32, 4, 1)])
     assert np.array_equal(res.histogram, hist) and res.bins == bins
     assert np.array_equal(np.stack(res.slicemaps[8].atlases), np.stack(atl[0]))
+
+
+# ---------------------------------------------------------------- preview builders (SURVEY s8 f)
+
+@pytest.fixture(scope="module")
+def golden_dp():
+    from pathlib import Path
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_datapreview.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_build_data_preview_golden(P, golden_dp):
+    """pipeline.py:240-257 (reference outputs on two mounted phantoms, incl. a 272->256 general ratio)."""
+    for i in range(int(golden_dp["dp_n"])):
+        dp = P.build_data_preview(P.Volume(golden_dp[f"dp{i}_in"]))
+        assert list(dp.filtered_bins) == golden_dp[f"dp{i}_bins"].tolist(), i
+        assert np.array_equal(np.stack(dp.slicemaps.atlases), golden_dp[f"dp{i}_atlases"]), i
+        assert dp.stages == ("slicemaps_conversion", "histogram_filtering")
+
+
+def test_acceptance_snapshot_36_views(P, golden, golden_dp):
+    """test_acceptance.py:217-244: 36 views, 256^2, 256 steps -> azimuth 250.0, H = 0.840239."""
+    snap = P.optimal_snapshot(P.Volume(golden["lphantom"]), n_views=36,
+                              params=P.ViewParams(image_dim=256, steps=256, mode="surface", threshold=60))
+    assert snap.azimuth_deg == 250.0 == float(golden_dp["acc_snap_az"])
+    assert snap.entropy == float(golden_dp["acc_snap_h"]) and abs(snap.entropy - 0.840239) <= 1e-5
+    assert np.array_equal(np.array(snap.per_view), golden_dp["acc_snap_per_view"])
+    assert np.array_equal(snap.image, golden_dp["acc_snap_img"])

@@ -8,6 +8,7 @@
 from __future__ import annotations
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -181,3 +182,12 @@ def test_extension_rescale_rule():
     assert np.all(np.diff(r.astype(int)) >= 0)
     lut = O.lut_u16({0, 5, 4095})
     assert lut[0] == 0 and lut[5] == 0 and lut[4095] == 0 and lut[4094] == r[4094]
+
+
+def test_data_preview_golden():
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_datapreview.npz") as z:
+        g = {k: z[k] for k in z.files}
+    for i in range(int(g["dp_n"])):
+        bins, atl = O.build_data_preview(g[f"dp{i}_in"])
+        assert list(bins) == g[f"dp{i}_bins"].tolist()
+        assert np.array_equal(np.stack(atl), g[f"dp{i}_atlases"])
