@@ -189,6 +189,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int rows_u = g.ty / UZ;
   const int units = (TZ / UZ) * rows_u * g.txu;
   const int s1_row = g.txu * L1PU;  // level-1 sums per (z1, y1) row of the tile
+  // Bank swizzle of the level-1 sums: the 4 lanes of a level-3 group read rows
+  // (z1, y1) that are whole 1-KB rows apart (same banks); XOR-ing x1 with a
+  // per-row 16-element (32-byte) offset taken from bit 1 of y1 and of z1 puts
+  // them in 4 different bank quarters.  Needs rows of whole 64-element blocks.
+  const int swz_mask = (s1_row & 63) == 0 ? 0x30 : 0;
+  auto s1_swz = [&](int z1, int y1) -> int { return ((((y1 >> 1) & 1) | (((z1 >> 1) & 1) << 1)) << 4) & swz_mask; };
 
   // this CTA's contiguous range of tiles (coordinates advance incrementally)
   const int per = g.n_tiles / gridDim.x, extra = g.n_tiles % gridDim.x;
@@ -269,8 +275,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       c_z2 = 2 * z3 + (q >> 1);
       c_y2 = 2 * y3 + (q & 1);
       c_x2 = 2 * x3;
-      // first level-1 child row (z1 = 2 z2, y1 = 2 y2), x1 = 2 x2 .. 2 x2 + 3
-      c_s1 = s1a + 2u * (uint32_t)(((2 * c_z2) * rows_u + 2 * c_y2) * s1_row + 2 * c_x2);
+      // first level-1 child row (z1 = 2 z2, y1 = 2 y2), x1 = 2 x2 .. 2 x2 + 3 (swizzled, see s1_swz)
+      c_s1 = s1a + 2u * (uint32_t)(((2 * c_z2) * rows_u + 2 * c_y2) * s1_row +
+                                   ((2 * c_x2) ^ s1_swz(2 * c_z2, 2 * c_y2)));
     }
   }
   __syncthreads();
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if constexpr (L >= 2) {
           // s1 layout [zr][yr][x1], x1 = xu*L1PU + j
-          uint16_t* d = s1k + (zr * rows_u + yr) * s1_row + xu * L1PU;
+          uint16_t* d = s1k + (zr * rows_u + yr) * s1_row + ((xu * L1PU) ^ s1_swz(zr, yr));
           if constexpr (L1PU == 8) *reinterpret_cast<uint4*>(d) = make_uint4(pr[0], pr[1], pr[2], pr[3]);
           else *reinterpret_cast<uint2*>(d) = make_uint2(pr[0], pr[1]);
         }
@@ -383,7 +390,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ez = 0; ez < 2; ez++)
 #pragma unroll
           for (int ey = 0; ey < 2; ey++) {
-            const uint32_t pair = *reinterpret_cast<const uint32_t*>(s1k + (ez * rows_u + 2 * y2 + ey) * s1_row + 2 * x2);
+            const uint32_t pair = *reinterpret_cast<const uint32_t*>(
+                s1k + (ez * rows_u + 2 * y2 + ey) * s1_row + ((2 * x2) ^ s1_swz(ez, 2 * y2 + ey)));
             sum += (pair & 0xFFFFu) + (pair >> 16);
           }
         if (want2) a.lv[2].out[level_offset<POW2>(a.lv[2], z0 >> 2, gy, gx)] = (uint8_t)((sum + 32) >> 6);
