@@ -226,6 +226,7 @@ def main():
     ap.add_argument("--no-mip", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mip-batches", type=int, default=2)
+    ap.add_argument("--no-configs", action="store_true", help="skip the c1 / c3 / c4-alpha side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -369,6 +370,10 @@ def main():
         del slab
         torch.cuda.empty_cache()
         mip = bench_mip(args, device, rank, world, dist)
+    others = None
+    if not args.no_configs and world == 1:
+        torch.cuda.empty_cache()
+        others = bench_other_configs(device)
 
     if rank == 0:
         line = {
@@ -388,6 +393,7 @@ def main():
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "mip": mip,
+            "other_configs": others,
         }
         print(json.dumps(line))
     if world > 1:
@@ -434,6 +440,74 @@ def bench_mip(args, device, rank, world, dist):
             "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames, image rows split across ranks"}
+
+
+def _time_steps(fn, reps: int, warmup: int = 2):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def bench_other_configs(device):
+    """Side measurements on the other BASELINE configs (same kernels, 1 GPU):
+    c1 (256^3 u8, one 16x16-grid 4096^2 atlas), c3 (2048^3 12-bit u16, 4 levels +
+    atlases, 16 GiB), c4 alpha compositing frames/s."""
+    import math
+    import torch
+    from paper_2311_15038_b200 import device as dev, synth
+    from paper_2311_15038_b200.device import AtlasSpec
+    from paper_2311_15038_b200.pipeline import plan_preview, run_preview
+    from paper_2311_15038_b200.types import ViewParams, plan_scheme
+    peak = _peaks()[0]["hbm_gbs"]
+    out = {}
+    # c1
+    spec = synth.config("c1")
+    vol = synth.generate(spec, device=device)
+    plan = plan_preview(spec.shape, {256: AtlasSpec(256, 4096, 16, 1)})
+    res = run_preview(vol, plan)
+    ms = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 200)
+    n = vol.numel()
+    out["c1"] = {"workload": "256^3 u8: hist + artifact-bin filter + one 16x16-grid 4096^2 atlas", "ms_per_step": ms,
+                 "gvoxel_per_s": n / ms / 1e6, "alg_bytes": 2 * n, "frac_of_hbm_peak": 2 * n / (ms * 1e-3) / 1e9 / peak,
+                 "note": "32 MB working set: launch/L2-bound (SURVEY s8 d); 2 launches per step"}
+    del vol, res
+    # c3
+    spec = synth.config("c3")
+    vol = synth.generate(spec, device=device)
+    schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec.of(plan_scheme(512)),
+               256: AtlasSpec.of(plan_scheme(256)), 128: AtlasSpec.of(plan_scheme(128))}
+    plan = plan_preview(spec.shape, schemes)
+    res = run_preview(vol, plan)
+    ms = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 10)
+    n = vol.numel()
+    alg = 2 * n + sum(t.numel() for t in res.atlases.values())
+    out["c3"] = {"workload": "2048^3 12-bit u16 (16 GiB): 4096-bin hist + filter o rescale + 4-level pyramid + atlases "
+                             "(1024: 64 maps of 4x4 4096^2; 512/256/128 planned)", "ms_per_step": ms,
+                 "gvoxel_per_s": n / ms / 1e6, "alg_bytes": alg, "achieved_GBps": alg / (ms * 1e-3) / 1e9,
+                 "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak}
+    del vol, res
+    torch.cuda.empty_cache()
+    # c4 alpha
+    spec = synth.config("c4")
+    vol = synth.generate(spec, device=device)
+    steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * spec.shape[0])
+    views = [ViewParams(azimuth_deg=10.0 * k, image_dim=1024, steps=steps, mode="alpha") for k in range(36)]
+    img = dev.render(vol, views, channels=4, fp32=True)
+    ms = _time_steps(lambda: dev.render(vol, views, channels=4, fp32=True, out=img), 2, warmup=1)
+    out["c4_alpha"] = {"workload": "36 azimuths x 1024^2 RGBA8, front-to-back alpha, 4-point TF, early stop 0.99, "
+                                   f"{steps} steps", "frames_per_s": 36 / (ms * 1e-3), "ms_per_frame": ms / 36}
+    del vol, img
+    torch.cuda.empty_cache()
+    return out
 
 
 if __name__ == "__main__":
