@@ -460,7 +460,7 @@ def _time_steps(fn, reps: int, warmup: int = 2):
 def bench_other_configs(device):
     """Side measurements on the other BASELINE configs (same kernels, 1 GPU):
     c1 (256^3 u8, one 16x16-grid 4096^2 atlas), c3 (2048^3 12-bit u16, 4 levels +
-    atlases, 16 GiB), c4 alpha compositing frames/s."""
+    atlases, 16 GiB), c4 alpha compositing frames/s, c5 volumes/min."""
     import math
     import torch
     from paper_2311_15038_b200 import device as dev, synth
@@ -506,6 +506,18 @@ def bench_other_configs(device):
     out["c4_alpha"] = {"workload": "36 azimuths x 1024^2 RGBA8, front-to-back alpha, 4-point TF, early stop 0.99, "
                                    f"{steps} steps", "frames_per_s": 36 / (ms * 1e-3), "ms_per_frame": ms / 36}
     del vol, img
+    torch.cuda.empty_cache()
+    # c5: stream of 1536^2 x 2048 u16 volumes, one GPU (replicas across GPUs)
+    from paper_2311_15038_b200.stream import PreviewStream
+    spec = synth.config("c5", seed=0)
+    vol = synth.generate(spec, device=device)
+    ps = PreviewStream(spec.shape, torch.uint16, device=device)
+    ms = _time_steps(lambda: ps.process(vol), 4, warmup=1)
+    n = vol.numel()
+    out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume: hist + filter o rescale + L1..L4 padded "
+                             "atlases + 36-view 512^2 MIP strip (from L2), one volume per GPU",
+                 "ms_per_volume": ms, "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6}
+    del vol, ps
     torch.cuda.empty_cache()
     return out
 

@@ -367,3 +367,35 @@ def test_acceptance_snapshot_36_views(P, golden, golden_dp):
     assert snap.entropy == float(golden_dp["acc_snap_h"]) and abs(snap.entropy - 0.840239) <= 1e-5
     assert np.array_equal(np.array(snap.per_view), golden_dp["acc_snap_per_view"])
     assert np.array_equal(snap.image, golden_dp["acc_snap_img"])
+
+
+# ---------------------------------------------------------------- config 5 stream (extension)
+
+def test_stream_c5_shape_reduced(P, cuda):
+    """Config-5 processing (u16 anisotropic, levels -> padded atlases, 36-view MIP
+    strip) at 1/8 scale against the oracle: histogram, LUT and every atlas
+    bit-exact, thumbnails within 1/255."""
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.stream import PreviewStream, scheme_for
+    spec = synth.small((256, 192, 192), dtype="u16", seed=21, n_shells=4)
+    vol = synth.generate(spec, device=cuda)
+    ps = PreviewStream(spec.shape, torch.uint16, thumb_dim=64, n_views=6, device=cuda)
+    res = ps.process(vol)
+    vox = vol.cpu().numpy()
+    hist, bins, f, _, _ = O.preview_pipeline(vox, [])
+    assert np.array_equal(res.hist.cpu().numpy(), hist)
+    assert set(np.nonzero(res.flags.cpu().numpy())[0].tolist()) == set(bins)
+    nz, ny, nx = vox.shape
+    for l, sp in ps.levels.items():
+        lv = O.downscale(f, (nx >> l, ny >> l, nz >> l))
+        want = np.stack(O.encode_slicemaps(O.pad_to_cube(lv, sp.s), (sp.s, sp.atlas_dim, sp.grid, sp.map_count)))
+        assert np.array_equal(res.atlases[l].cpu().numpy(), want), l
+        if l == ps.thumb_level:
+            thumb_src = lv
+    assert ps.thumb_shape == thumb_src.shape
+    for k, view in enumerate(ps.views):
+        ref = O.render_mip(thumb_src, view.azimuth_deg, view.image_dim, view.steps)
+        got = res.thumbs[k].cpu().numpy()
+        assert int(np.abs(got[..., 0].astype(int) - ref).max()) <= 1
+        assert (got[..., 3] == 255).all()
+    assert scheme_for((1024, 768, 768)) == (1024, 4096, 4, 64) or scheme_for((1024, 768, 768)).s == 1024
