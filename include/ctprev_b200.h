@@ -145,6 +145,12 @@ int ctp_encode_atlas_u8(const uint8_t* cube, int64_t nz, int64_t ny, int64_t nx,
                         int32_t s, int32_t grid, int32_t atlas_dim, int32_t map_count,
                         uint8_t* atlases, void* stream);
 
+/* Replaces mask.py:194-212 apply_circle_mask: out = in where (x - cx)^2 +
+ * (y - cy)^2 <= r_eff_sq (fp64, no FMA contraction: numpy's exact predicate),
+ * else 0, on every slice.  r_eff_sq = (r * (1 - margin))**2 from the host. */
+int ctp_circle_mask_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, double cx, double cy,
+                       double r_eff_sq, uint8_t* out, void* stream);
+
 /* Inverse (slicemap.py:145-155 decode_slicemaps): atlases -> s^3 cube. */
 int ctp_decode_atlas_u8(const uint8_t* atlases, int32_t s, int32_t grid, int32_t atlas_dim,
                         int32_t map_count, uint8_t* cube, void* stream);

@@ -16,7 +16,7 @@ no CPU fallback.  ``install()`` rebinds these functions inside an imported
 from .errors import *  # noqa: F401,F403
 from .types import (ADDITIVE, ALPHA, MIP, SURFACE, EntropyResult, Histogram256, SlicemapScheme, SlicemapSet,
                     SnapshotResult, ViewParams, Volume, plan_scheme, slice_cell)
-from .ops import (PreviewResult, artifact_bins, build_data_preview, decode_slicemaps, downscale_volume, encode_slicemaps,
+from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, decode_slicemaps, downscale_volume, encode_slicemaps,
                   filter_histogram_bins, image_entropy, optimal_snapshot, preview_pipeline, render_view,
                   render_views, volume_histogram)
 from .install import install, uninstall
@@ -28,5 +28,5 @@ __all__ = [
     "SnapshotResult", "SURFACE", "ADDITIVE", "MIP", "ALPHA", "plan_scheme", "slice_cell",
     "volume_histogram", "artifact_bins", "filter_histogram_bins", "downscale_volume", "encode_slicemaps",
     "decode_slicemaps", "render_view", "render_views", "image_entropy", "optimal_snapshot",
-    "preview_pipeline", "PreviewResult", "build_data_preview", "install", "uninstall",
+    "preview_pipeline", "PreviewResult", "build_data_preview", "apply_circle_mask", "install", "uninstall",
 ]

@@ -79,6 +79,24 @@ __global__ void decode_atlas_kernel(const uint8_t* __restrict__ atlases, int s, 
   }
 }
 
+// mask.py:208-211 apply_circle_mask: keep (x, y) iff (x - cx)^2 + (y - cy)^2 <= r_eff^2,
+// evaluated in fp64 with explicit round-to-nearest products/sums (no FMA
+// contraction), i.e. exactly numpy's (ix - cx)**2 + (iy - cy)**2 <= r_eff**2.
+__device__ __forceinline__ bool in_circle(int64_t x, int64_t y, double cx, double cy, double r2) {
+  const double dx = __dsub_rn((double)x, cx), dy = __dsub_rn((double)y, cy);
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= r2;
+}
+
+__global__ void circle_mask_kernel(const uint8_t* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, double cx,
+                                   double cy, double r2, uint8_t* __restrict__ out) {
+  const int64_t total = nz * ny * nx;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = o % nx;
+    const int64_t y = (o / nx) % ny;
+    out[o] = in_circle(x, y, cx, cy, r2) ? __ldg(in + o) : (uint8_t)0;
+  }
+}
+
 static int grid1d(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms() * 16;
@@ -122,6 +140,19 @@ int ctp_encode_atlas_u8(const uint8_t* cube, int64_t nz, int64_t ny, int64_t nx,
   encode_atlas_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(cube, nz, ny, nx, s, grid, atlas_dim,
                                                                          map_count, atlases);
   CTP_CUDA_CHECK_LAUNCH("encode_atlas_kernel");
+  return CTP_OK;
+}
+
+int ctp_circle_mask_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, double cx, double cy, double r_eff_sq,
+                       uint8_t* out, void* stream) {
+  CTP_REQUIRE(in && out, CTP_E_INVALID, "ctp_circle_mask_u8: null pointer");
+  CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1, CTP_E_INVALID, "ctp_circle_mask_u8: degenerate shape");
+  // mask.py:202-205 (the radius / margin checks stay with the caller, which holds the Circle)
+  CTP_REQUIRE(0.0 <= cx && cx < (double)nx && 0.0 <= cy && cy < (double)ny, CTP_E_INVALID,
+              "center (%.1f, %.1f) outside %lldx%lld slice", cx, cy, (long long)nx, (long long)ny);
+  const int64_t total = nx * ny * nz;
+  circle_mask_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(in, nz, ny, nx, cx, cy, r_eff_sq, out);
+  CTP_CUDA_CHECK_LAUNCH("circle_mask_kernel");
   return CTP_OK;
 }
 

@@ -302,3 +302,14 @@ def synth(shape, dtype, seed: int, bg_mean: float, bg_sd: float, shells, speckle
     _lib.call("ctp_synth_volume", _ptr(out), elem, nz, ny, nx, z_base, full_nz, seed, bg_mean, bg_sd, vmax,
               arr, len(shells), speckle_p, _stream())
     return out
+
+
+def circle_mask(vol: torch.Tensor, cx: float, cy: float, r_eff_sq: float, out: torch.Tensor | None = None):
+    """mask.py:208-211 on the device (every slice)."""
+    _check_dev(vol, torch.uint8, "circle_mask")
+    nz, ny, nx = vol.shape
+    if out is None:
+        out = torch.empty_like(vol)
+    _lib.call("ctp_circle_mask_u8", _ptr(vol), nz, ny, nx, float(cx), float(cy), float(r_eff_sq), _ptr(out),
+              _stream())
+    return out

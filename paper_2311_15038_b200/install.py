@@ -26,6 +26,7 @@ BINDINGS = {
     "image_entropy": ["render", "cli", ""],
     "optimal_snapshot": ["render", "pipeline", "cli", ""],
     "build_data_preview": ["pipeline", ""],
+    "apply_circle_mask": ["mask", "pipeline", "cli", ""],
 }
 
 _saved: dict = {}

@@ -323,3 +323,17 @@ def build_data_preview(volume):
     bins = tuple(int(b) for b in np.nonzero(_host(flags))[0])
     sset = FACTORY.SlicemapSet(scheme=scheme, atlases=tuple(a[m] for m in range(spec.map_count)))
     return FACTORY.DataPreview(slicemaps=sset, filtered_bins=bins, stages=STAGES_DATA)
+
+
+def apply_circle_mask(volume, circle, margin: float = 0.02):
+    """mask.py:194-212: zero every voxel outside the circle shrunk by ``margin``."""
+    from .errors import CircleOutOfBounds
+    vox = _voxels(volume)
+    nz, ny, nx = vox.shape
+    if not (0 <= circle.cx < nx and 0 <= circle.cy < ny):                   # mask.py:202-205
+        raise CircleOutOfBounds(f"center ({circle.cx:.1f}, {circle.cy:.1f}) outside {nx}x{ny} slice")
+    if not 0.0 <= margin < 1.0:                                              # mask.py:206-207
+        raise RangeOutOfBounds(f"margin {margin} outside [0, 1)")
+    r_eff = circle.r * (1.0 - margin)                                        # mask.py:208
+    out = dev.circle_mask(to_device(vox), circle.cx, circle.cy, r_eff ** 2)
+    return FACTORY.Volume(_host(out), getattr(volume, "voxel_size_um", None))

@@ -174,6 +174,17 @@ def data_preview_golden() -> None:
     g["acc_snap_h"] = np.array(snap.entropy)
     g["acc_snap_per_view"] = np.array(snap.per_view, dtype=np.float64)
     g["acc_snap_img"] = snap.image
+    # apply_circle_mask (mask.py:194-212), fractional centres, margins, boundary-touching radii
+    from ctprev.mask import Circle, apply_circle_mask
+    rng = np.random.default_rng(77)
+    mvol = rng.integers(1, 256, size=(3, 57, 63), dtype=np.uint8)
+    cases = [(31.0, 28.0, 20.0, 0.02), (30.5, 27.25, 26.0, 0.0), (12.3, 40.7, 33.3, 0.1), (0.0, 0.0, 70.0, 0.5),
+             (62.9, 56.9, 5.0, 0.02)]
+    for i, (cx, cy, r, m) in enumerate(cases):
+        g[f"cm{i}_params"] = np.array([cx, cy, r, m])
+        g[f"cm{i}_out"] = apply_circle_mask(Volume(mvol), Circle(cx, cy, r), margin=m).voxels.copy()
+    g["cm_in"] = mvol
+    g["cm_n"] = np.array(len(cases))
     np.savez_compressed(out, **g)
     print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
 

@@ -399,3 +399,17 @@ def test_stream_c5_shape_reduced(P, cuda):
         assert int(np.abs(got[..., 0].astype(int) - ref).max()) <= 1
         assert (got[..., 3] == 255).all()
     assert scheme_for((1024, 768, 768)) == (1024, 4096, 4, 64) or scheme_for((1024, 768, 768)).s == 1024
+
+
+def test_apply_circle_mask_golden(P, golden_dp):
+    """mask.py:194-212 (exact fp64 predicate incl. points on the boundary) + its errors."""
+    from types import SimpleNamespace as C
+    vol = P.Volume(golden_dp["cm_in"])
+    for i in range(int(golden_dp["cm_n"])):
+        cx, cy, r, m = golden_dp[f"cm{i}_params"]
+        out = P.apply_circle_mask(vol, C(cx=float(cx), cy=float(cy), r=float(r)), margin=float(m))
+        assert np.array_equal(out.voxels, golden_dp[f"cm{i}_out"]), i
+    with pytest.raises(P.CircleOutOfBounds):
+        P.apply_circle_mask(vol, C(cx=63.0, cy=1.0, r=5.0))
+    with pytest.raises(P.RangeOutOfBounds):
+        P.apply_circle_mask(vol, C(cx=3.0, cy=1.0, r=5.0), margin=1.0)

@@ -191,3 +191,11 @@ def test_data_preview_golden():
         bins, atl = O.build_data_preview(g[f"dp{i}_in"])
         assert list(bins) == g[f"dp{i}_bins"].tolist()
         assert np.array_equal(np.stack(atl), g[f"dp{i}_atlases"])
+
+
+def test_circle_mask_golden():
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_datapreview.npz") as z:
+        g = {k: z[k] for k in z.files}
+    for i in range(int(g["cm_n"])):
+        cx, cy, r, m = g[f"cm{i}_params"]
+        assert np.array_equal(O.apply_circle_mask(g["cm_in"], cx, cy, r, m), g[f"cm{i}_out"]), i

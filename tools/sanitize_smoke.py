@@ -1,0 +1,44 @@
+"""Small calls of every kernel, for compute-sanitizer (memcheck / racecheck / synccheck).
+
+usage: compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2311_15038_b200 as P  # noqa: E402
+from paper_2311_15038_b200 import device as dev, synth  # noqa: E402
+from paper_2311_15038_b200.device import AtlasSpec  # noqa: E402
+from paper_2311_15038_b200.stream import PreviewStream  # noqa: E402
+
+torch.cuda.set_device(0)
+# fused pass, u8, levels 0..3 (atlases + dense), partial tiles (ny not a multiple of the tile height)
+v8 = synth.generate(synth.small((64, 72, 96), seed=1))
+lut, flags = dev.artifact_lut_fused(v8)
+hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+dev.preview(v8, lut, {0: "xyz", 1: AtlasSpec(64, 512, 8, 1), 2: "xyz", 3: AtlasSpec(16, 64, 4, 1)}, hist=hist)
+# u16, level 4
+v16 = synth.generate(synth.small((64, 64, 128), dtype="u16", seed=2))
+lut16, _ = dev.artifact_lut_fused(v16)
+h16 = torch.zeros(4096, dtype=torch.int64, device="cuda")
+dev.preview(v16, lut16, {1: "xyz", 4: AtlasSpec(8, 32, 4, 1)}, hist=h16)
+# stand-alone kernels
+dev.hist_u8(v8, (3, 40))
+dev.lut_apply_u8(v8[:, :, :37].contiguous(), lut, hist=hist)
+dev.downscale(v8, (37, 29, 23))
+dev.encode_atlas(v8[:48, :48, :48].contiguous(), AtlasSpec(64, 512, 8, 1))
+dev.decode_atlas(dev.encode_atlas(v8[:64, :64, :64].contiguous(), AtlasSpec(64, 512, 8, 1)), AtlasSpec(64, 512, 8, 1))
+# renders: exact fp64 modes, fp32 MIP (row planes) and alpha (texture)
+for m in ("surface", "additive"):
+    dev.render(v8, [P.ViewParams(azimuth_deg=a, image_dim=32, steps=48, mode=m, threshold=60) for a in (0.0, 37.0)])
+dev.render(v8, [P.ViewParams(azimuth_deg=15.0, image_dim=32, steps=48, mode="mip")], channels=4, fp32=True)
+dev.render(v8, [P.ViewParams(azimuth_deg=15.0, image_dim=32, steps=48, mode="alpha")], channels=4, fp32=True)
+dev.image_hist(torch.zeros((3, 16, 16), dtype=torch.uint8, device="cuda"))
+# config-5 stream processor at a small shape
+ps = PreviewStream((128, 96, 96), torch.uint16, thumb_dim=32, n_views=2)
+ps.process(synth.generate(synth.small((128, 96, 96), dtype="u16", seed=3)))
+torch.cuda.synchronize()
+print("sanitize smoke done", int(hist.sum().item()), int(h16.sum().item()))
