@@ -386,7 +386,8 @@ def main():
                        "l2": "input 1 GiB per step > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "kernel": "preview_kernel<uint8_t,3,1024 thr> (fused)", "kernel_ms": kmean,
+                         "kernel": "preview_kernel<uint8_t,3,1024 thr>: the whole step in one cooperative launch "
+                                   "(artifact-LUT phase + fused hist/filter/pyramid/atlas pass)", "kernel_ms": kmean,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -129,6 +129,20 @@ int ctp_preview_u16(const uint16_t* vol, int64_t nz, int64_t ny, int64_t nx, int
                     const uint8_t* lut4096, int32_t nlev, const ctp_level_out* levels,
                     uint64_t* hist4096, void* stream);
 
+/* The whole preview step of a full volume in ONE cooperative launch: the
+ * artifact-LUT step of ctp_artifact_lut (top n_top slices of this volume,
+ * cutoff_floor, the identity LUT for u8 / filter o rescale for u16) runs inside
+ * the fused pass while its first tiles are already streaming in (one grid
+ * barrier), then the pass of ctp_preview_u8 / _u16 with that LUT.  hist is
+ * zeroed by the launch; lut_out / flags_out (optional) receive the LUT and the
+ * artifact-bin flags; workspace: uint64[4097], zero on entry, left zero. */
+int ctp_preview_step_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, int32_t n_top,
+                        uint64_t cutoff_floor, int32_t nlev, const ctp_level_out* levels, uint64_t* hist,
+                        uint8_t* lut_out, uint8_t* flags_out, uint64_t* workspace, void* stream);
+int ctp_preview_step_u16(const uint16_t* vol, int64_t nz, int64_t ny, int64_t nx, int32_t n_top,
+                         uint64_t cutoff_floor, int32_t nlev, const ctp_level_out* levels, uint64_t* hist4096,
+                         uint8_t* lut_out, uint8_t* flags_out, uint64_t* workspace, void* stream);
+
 /* ---------------- general resampling / atlas packing -------------------- */
 
 /* Replaces volume.py:277-309 downscale_volume for ANY target (half-open

@@ -82,6 +82,8 @@ SIGNATURES = {
     "ctp_artifact_lut": [_P, _I32, _I64, _I64, _I64, _I32, C.c_uint64, _I32, _P, _P, _P, _P, _P],
     "ctp_preview_u8": [_P, _I64, _I64, _I64, _I64, _P, _I32, C.POINTER(LevelOut), _P, _P],
     "ctp_preview_u16": [_P, _I64, _I64, _I64, _I64, _P, _I32, C.POINTER(LevelOut), _P, _P],
+    "ctp_preview_step_u8": [_P, _I64, _I64, _I64, _I32, C.c_uint64, _I32, C.POINTER(LevelOut), _P, _P, _P, _P, _P],
+    "ctp_preview_step_u16": [_P, _I64, _I64, _I64, _I32, C.c_uint64, _I32, C.POINTER(LevelOut), _P, _P, _P, _P, _P],
     "ctp_downscale_u8": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P],
     "ctp_encode_atlas_u8": [_P, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P],
     "ctp_decode_atlas_u8": [_P, _I32, _I32, _I32, _I32, _P, _P],

@@ -35,6 +35,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cooperative_groups.h>
 #include "ctp_common.cuh"
 
 namespace ctp {
@@ -67,6 +68,14 @@ struct PvArgs {
   unsigned long long* hist;
   LevelDst lv[CTP_MAX_LEVELS];
   PvGeom g;
+  // in-kernel artifact LUT (the whole step in ONE cooperative launch) when top != nullptr
+  const void* top;                 // the top n_top slices (mask.py:227), 16-byte aligned
+  int64_t top_n;                   // elements in the top slab
+  unsigned long long cutoff_floor; // floor(frac * top.size), mask.py:229-230
+  int32_t vmax;                    // 0: identity LUT (u8); > 0: filter o 16->8 rescale
+  uint8_t* lut_out;                // optional copies for the host
+  uint8_t* flags_out;
+  unsigned long long* ws;          // uint64[4097], zero on entry, left zero
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -223,10 +232,66 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < NST; s++)
       if (t_begin + s < t_end) issue(t_begin + s, s);
 
+  __shared__ uint8_t slut[Vox<T>::NBINS];
+  if (a.top != nullptr) {
+    // ---- the artifact-LUT step inside this launch (mask.py:215-231, 241-245):
+    // the first tiles are already streaming in while every CTA histograms its
+    // share of the top slab; one grid barrier; every CTA derives the LUT.
+    constexpr int NB = Vox<T>::NBINS;
+    for (int i = threadIdx.x; i < NB; i += THREADS) hs[i] = 0;
+    __syncthreads();
+    const int64_t nvec = a.top_n / UXW;  // 16-byte vectors (rows are 16-byte aligned)
+    const int64_t per_cta = (nvec + gridDim.x - 1) / gridDim.x;
+    const int64_t v0 = blockIdx.x * per_cta, v1 = min(nvec, v0 + per_cta);
+    const uint4* tp = reinterpret_cast<const uint4*>(a.top);
+    for (int64_t i = v0 + threadIdx.x; i < v1; i += THREADS) {
+      const uint4 q = __ldcs(tp + i);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if constexpr (sizeof(T) == 1) {
+#pragma unroll
+          for (int b = 0; b < 4; b++) atomicAdd(&hs[(w[k] >> (8 * b)) & 255u], 1u);
+        } else {
+          atomicAdd(&hs[min(w[k] & 0xFFFFu, 4095u)], 1u);
+          atomicAdd(&hs[min(w[k] >> 16, 4095u)], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NB; b += THREADS)
+      if (hs[b]) atomicAdd(a.ws + b, (unsigned long long)hs[b]);
+    if (blockIdx.x == 0 && a.hist)
+      for (int b = threadIdx.x; b < NB; b += THREADS) a.hist[b] = 0;  // before any CTA can flush into it
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    for (int b = threadIdx.x; b < NB; b += THREADS) {
+      const unsigned long long c = __ldcg(a.ws + b);
+      const bool flagged = (b == 0) || (c > a.cutoff_floor);  // mask.py:230-231
+      uint32_t val = (uint32_t)b;
+      if (a.vmax > 0) {
+        const uint32_t v = min((uint32_t)b, (uint32_t)a.vmax);
+        val = (uint32_t)((2ull * 255ull * v + (uint64_t)a.vmax) / (2ull * (uint64_t)a.vmax));
+      }
+      slut[b] = flagged ? 0 : (uint8_t)val;
+      if (blockIdx.x == 0) {
+        if (a.lut_out) a.lut_out[b] = slut[b];
+        if (a.flags_out) a.flags_out[b] = flagged ? 1 : 0;
+      }
+    }
+    __shared__ bool last_reader;
+    __syncthreads();
+    if (threadIdx.x == 0) last_reader = atomicAdd(a.ws + 4096, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (last_reader) {  // every CTA has read ws: reset it for the next call
+      for (int b = threadIdx.x; b < NB; b += THREADS) a.ws[b] = 0;
+      if (threadIdx.x == 0) a.ws[4096] = 0;
+    }
+  }
   // counter words: LUT value in the low byte, count 0
   for (int i = threadIdx.x; i < HW; i += THREADS) {
     const int bin = (sizeof(T) == 2) ? i : (i >> 5);
-    hs[i] = a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255);
+    hs[i] = a.top ? (uint32_t)slut[bin] : (a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255));
   }
   const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
   const uint32_t lb = (sizeof(T) == 2) ? tbl : tbl + 4u * (uint32_t)lane;
@@ -525,9 +590,24 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
 template <typename T, int L, int THREADS, int NST, int MAXU, bool WANT0, bool POW2>
 static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
   constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
-  static_assert(sm <= 227 * 1024, "shared memory budget");
+  static_assert(sm <= 227 * 1024 - 4096, "shared memory budget");
   auto kern = preview_kernel<T, L, THREADS, NST, MAXU, WANT0, POW2>;
   CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  if (a.top != nullptr) {
+    // the in-kernel LUT step has one grid barrier: a cooperative launch
+    // guarantees every CTA is resident (one per SM here)
+    int per_sm = 0;
+    CTP_CUDA_CALL(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, sm));
+    CTP_REQUIRE(per_sm >= 1, CTP_E_CUDA, "preview: kernel does not fit on an SM");
+    if (grid > per_sm * num_sms()) grid = per_sm * num_sms();
+    CUtensorMap map_copy = map;
+    PvArgs a_copy = a;
+    void* params[] = {&map_copy, &a_copy};
+    CTP_CUDA_CALL(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(THREADS), params,
+                                              sm, st));
+    ++launch_counter();
+    return CTP_OK;
+  }
   kern<<<grid, THREADS, sm, st>>>(map, a);
   CTP_CUDA_CHECK_LAUNCH("preview_kernel");
   return CTP_OK;
@@ -587,9 +667,18 @@ static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
   }
 }
 
+struct AutoLut {  // the artifact-LUT step fused into the launch (ctp_preview_step_*)
+  int n_top;
+  uint64_t cutoff_floor;
+  uint8_t* lut_out;
+  uint8_t* flags_out;
+  uint64_t* workspace;
+};
+
 template <typename T>
 static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_t z_base, const uint8_t* lut,
-                        int nlev, const ctp_level_out* levels, uint64_t* hist, void* stream) {
+                        int nlev, const ctp_level_out* levels, uint64_t* hist, void* stream,
+                        const AutoLut* autolut = nullptr) {
   constexpr int UXW = Vox<T>::UXW;
   CTP_REQUIRE(vol != nullptr && levels != nullptr, CTP_E_INVALID, "preview: null pointer");
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1, CTP_E_INVALID, "preview: degenerate shape");
@@ -619,6 +708,25 @@ static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_
   a.g.nx = (int)nx;
   a.g.ny = (int)ny;
   a.g.nz = (int)nz;
+  a.top = nullptr;
+  a.top_n = 0;
+  a.cutoff_floor = 0;
+  a.vmax = 0;
+  a.lut_out = a.flags_out = nullptr;
+  a.ws = nullptr;
+  if (autolut != nullptr) {
+    CTP_REQUIRE(1 <= autolut->n_top && autolut->n_top <= nz, CTP_E_INVALID, "n_top %d outside [1, %lld]",
+                autolut->n_top, (long long)nz);  // mask.py:223-224
+    CTP_REQUIRE(autolut->workspace != nullptr, CTP_E_INVALID, "preview step: workspace required");
+    a.top = vol + (nz - autolut->n_top) * ny * nx;
+    a.top_n = (int64_t)autolut->n_top * ny * nx;
+    a.cutoff_floor = (unsigned long long)autolut->cutoff_floor;
+    a.vmax = sizeof(T) == 2 ? 4095 : 0;
+    a.lut_out = autolut->lut_out;
+    a.flags_out = autolut->flags_out;
+    a.ws = reinterpret_cast<unsigned long long*>(autolut->workspace);
+    a.lut = nullptr;
+  }
 
   cudaStream_t st = as_stream(stream);
   switch (nlev) {
@@ -637,6 +745,20 @@ extern "C" {
 int ctp_preview_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, int64_t z_base, const uint8_t* lut,
                    int32_t nlev, const ctp_level_out* levels, uint64_t* hist, void* stream) {
   return ctp::preview_impl<uint8_t>(vol, nz, ny, nx, z_base, lut, nlev, levels, hist, stream);
+}
+
+int ctp_preview_step_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, int32_t n_top, uint64_t cutoff_floor,
+                        int32_t nlev, const ctp_level_out* levels, uint64_t* hist, uint8_t* lut_out, uint8_t* flags_out,
+                        uint64_t* workspace, void* stream) {
+  const ctp::AutoLut al{n_top, cutoff_floor, lut_out, flags_out, workspace};
+  return ctp::preview_impl<uint8_t>(vol, nz, ny, nx, 0, nullptr, nlev, levels, hist, stream, &al);
+}
+
+int ctp_preview_step_u16(const uint16_t* vol, int64_t nz, int64_t ny, int64_t nx, int32_t n_top,
+                         uint64_t cutoff_floor, int32_t nlev, const ctp_level_out* levels, uint64_t* hist4096,
+                         uint8_t* lut_out, uint8_t* flags_out, uint64_t* workspace, void* stream) {
+  const ctp::AutoLut al{n_top, cutoff_floor, lut_out, flags_out, workspace};
+  return ctp::preview_impl<uint16_t>(vol, nz, ny, nx, 0, nullptr, nlev, levels, hist4096, stream, &al);
 }
 
 int ctp_preview_u16(const uint16_t* vol, int64_t nz, int64_t ny, int64_t nx, int64_t z_base, const uint8_t* lut4096,

@@ -304,6 +304,43 @@ def synth(shape, dtype, seed: int, bg_mean: float, bg_sd: float, shells, speckle
     return out
 
 
+def preview_step(vol: torch.Tensor, outputs: dict, n_top: int = 3, frac: float = 0.0005,
+                 hist: torch.Tensor | None = None, lut: torch.Tensor | None = None, flags: torch.Tensor | None = None,
+                 out_tensors: dict | None = None):
+    """The whole step of a full volume in ONE cooperative launch: artifact LUT of the
+    top ``n_top`` slices (mask.py:215-231) + the fused pass (``preview``).
+    Returns (outputs dict, hist, lut, flags); hist is zeroed by the launch."""
+    is16 = vol.dtype == torch.uint16
+    _check_dev(vol, torch.uint16 if is16 else torch.uint8, "preview_step")
+    nz, ny, nx = vol.shape
+    nbins = NBINS_U16 if is16 else NBINS_U8
+    if hist is None:
+        hist = torch.empty(nbins, dtype=torch.int64, device=vol.device)
+    if lut is None:
+        lut = torch.empty(nbins, dtype=torch.uint8, device=vol.device)
+    if flags is None:
+        flags = torch.empty(nbins, dtype=torch.uint8, device=vol.device)
+    nlev = max(outputs) if outputs else 0
+    levels = [None] * _lib.MAX_LEVELS
+    res = {}
+    for l, spec in outputs.items():
+        shape = (nz >> l, ny >> l, nx >> l)
+        t = out_tensors.get(l) if out_tensors else None
+        if t is None:
+            t = alloc_level(shape, spec, vol.device)
+        res[l] = t
+        if spec is None or spec == "xyz":
+            levels[l] = LevelOut(t.data_ptr(), _lib.LAYOUT_XYZ, 0, 0, 0, 0, 0)
+        else:
+            levels[l] = LevelOut(t.data_ptr(), _lib.LAYOUT_ATLAS, spec.s, spec.grid, spec.atlas_dim,
+                                 spec.map_count, 0)
+    fn = "ctp_preview_step_u16" if is16 else "ctp_preview_step_u8"
+    _lib.call(fn, _ptr(vol), nz, ny, nx, n_top, cutoff_floor(frac, n_top * ny * nx), nlev,
+              _lib.levels_array(levels), _ptr(hist), _ptr(lut), _ptr(flags), _ptr(_workspace(vol.device)),
+              _stream())
+    return res, hist, lut, flags
+
+
 def circle_mask(vol: torch.Tensor, cx: float, cy: float, r_eff_sq: float, out: torch.Tensor | None = None):
     """mask.py:208-211 on the device (every slice)."""
     _check_dev(vol, torch.uint8, "circle_mask")

@@ -132,6 +132,17 @@ class ShardedPreview:
         """slab: this rank's [z0, z1) voxels on ``device``.  Returns {hist, lut, atlases} (complete on rank 0)."""
         nz = self.shape[0]
         owner = self.world - 1
+        if self.world == 1 and isinstance(self.compute, DeviceSlabCompute):
+            # a single rank holds the whole volume: LUT step + fused pass in one cooperative launch
+            if self.fused_events is not None:
+                self.fused_events[0].record()
+            _, _, lut, _ = self.compute.dev.preview_step(
+                slab, self.compute.fused_levels, self.n_top, self.frac, hist=self.hist,
+                lut=getattr(self, "_lut_buf", None), out_tensors=self.atlases)
+            if self.fused_events is not None:
+                self.fused_events[1].record()
+            self._lut_buf = lut
+            return {"hist": self.hist, "lut": lut, "atlases": self.atlases}
         zeroed = False
         if self.rank == owner:
             top = slab[slab.shape[0] - self.n_top:]

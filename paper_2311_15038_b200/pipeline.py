@@ -90,19 +90,19 @@ class DevicePreview:
 
 def run_preview(vol: torch.Tensor, plan: PreviewPlan, n_top: int = 3, frac: float = 0.0005,
                 hist: torch.Tensor | None = None) -> DevicePreview:
-    """All device work for one volume on the current stream (no sync)."""
+    """All device work for one volume on the current stream (no sync).  ``hist``
+    (optional buffer to reuse) is zeroed and receives the histogram of ``vol``."""
     nbins = dev.NBINS_U8 if vol.dtype == torch.uint8 else dev.NBINS_U16
-    if hist is None:  # one launch: top-slab histogram + LUT + zeroing of the histogram
+    if hist is None:
         hist = torch.empty(nbins, dtype=torch.int64, device=vol.device)
-        lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
-    else:
-        lut, flags = dev.artifact_lut_fused(vol, n_top, frac)
     nz, ny, nx = vol.shape
     if vol.dtype == torch.uint8 and nx % 16 and set(plan.fused) == {0}:
         # rows not 16-byte vectorisable: filter + histogram with the any-size LUT kernel
+        lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
         outs = {0: dev.lut_apply_u8(vol, lut, hist=hist)}
     else:
-        outs = dev.preview(vol, lut, plan.fused, hist=hist)
+        # the whole step (artifact LUT + fused pass) in one cooperative launch
+        outs, hist, lut, flags = dev.preview_step(vol, plan.fused, n_top, frac, hist=hist)
     atlases, levels = {}, {}
     filtered = outs.get(0) if plan.fused.get(0) == "xyz" else None
     for s, l in plan.scheme_level.items():

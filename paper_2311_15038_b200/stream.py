@@ -76,12 +76,12 @@ class PreviewStream:
         self.thumbs = torch.empty((n_views, thumb_dim, thumb_dim, 4), dtype=torch.uint8, device=self.device)
 
     def process(self, vol: torch.Tensor) -> StreamResult:
-        lut, flags = dev.artifact_lut_fused(vol, 3, 0.0005, zero_hist=self.hist)
         outputs = dict(self.levels)
         outputs[self.thumb_level] = "xyz"       # the thumbnail level dense, its atlas packed from it
-        outs = dev.preview(vol, lut, outputs, hist=self.hist,
-                           out_tensors={l: t for l, t in self.atlases.items() if l != self.thumb_level}
-                           | {self.thumb_level: self.thumb_vol})
+        outs, _, lut, flags = dev.preview_step(
+            vol, outputs, 3, 0.0005, hist=self.hist,
+            out_tensors={l: t for l, t in self.atlases.items() if l != self.thumb_level}
+            | {self.thumb_level: self.thumb_vol})
         for l, t in outs.items():
             if l != self.thumb_level:
                 self.atlases[l] = t
