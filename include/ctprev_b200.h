@@ -200,6 +200,22 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx,
                   const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1,
                   uint8_t* out, void* stream);
 
+/* The same over a z-slab (sort-last at the reference's elevation-0 camera,
+ * render.py:131-140: image row j samples only the slices around one uz(j), so
+ * per-slab images are disjoint row bands).  `slab` holds slices
+ * [z_base, z_base + slab_nz) of an nz-deep volume; the geometry is the full
+ * volume's.  Every row in [row0, row1) must read only held slices (the
+ * trilinear pair, the surface gradient's +-1 and one slice of margin:
+ * [floor(uz)-2, floor(uz)+3]), else CTP_E_INVALID. */
+int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz,
+                       int64_t nz, int64_t ny, int64_t nx,
+                       const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1,
+                       uint8_t* out, void* stream);
+
+/* The fp32 MIP/alpha path keeps its per-row planes (2 B per voxel per image
+ * row) allocated between calls while the shape is unchanged; this frees them. */
+int ctp_render_release(void);
+
 /* Per-image 256-bin histograms for image_entropy (render.py:248-262):
  * hist[i*256 + b] = #pixels of image i equal to b (accumulated). */
 int ctp_image_hist_u8(const uint8_t* imgs, int32_t n_images, int64_t pixels,

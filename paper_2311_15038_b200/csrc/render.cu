@@ -19,6 +19,9 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <memory>
+#include <mutex>
+
 namespace ctp {
 
 struct RenderGeom {
@@ -32,6 +35,7 @@ struct ViewDev {
   float tf[4][5];
   double slope[3][4];  // (c_{j+1} - c_j) / (x_{j+1} - x_j) per segment and channel
   float early_stop;
+  float skip_lvl;  // alpha: 8.8 level at or below which the transfer function's alpha is 0 (-1: none)
 };
 
 constexpr int kMaxViews = 64;
@@ -40,7 +44,8 @@ struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per
 };
 
 template <typename R>
-__device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R uy, R uz, int nx, int ny, int nz) {
+__device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R uy, R uz, int nx, int ny, int nz,
+                                        int zb) {
   // render.py:68-111
   const R fx0 = floor(ux), fy0 = floor(uy), fz0 = floor(uz);
   int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
@@ -48,11 +53,12 @@ __device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R
   int x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
   x0 = min(max(x0, 0), nx - 1); y0 = min(max(y0, 0), ny - 1); z0 = min(max(z0, 0), nz - 1);
   x1 = min(max(x1, 0), nx - 1); y1 = min(max(y1, 0), ny - 1); z1 = min(max(z1, 0), nz - 1);
+  // vox holds slices [zb, ...) (a z-slab with its halo; zb = 0 for a whole volume)
   const int64_t sy = nx, sz = (int64_t)nx * ny;
-  const uint8_t* p00 = vox + z0 * sz + y0 * sy;
-  const uint8_t* p10 = vox + z0 * sz + y1 * sy;
-  const uint8_t* p01 = vox + z1 * sz + y0 * sy;
-  const uint8_t* p11 = vox + z1 * sz + y1 * sy;
+  const uint8_t* p00 = vox + (z0 - zb) * sz + y0 * sy;
+  const uint8_t* p10 = vox + (z0 - zb) * sz + y1 * sy;
+  const uint8_t* p01 = vox + (z1 - zb) * sz + y0 * sy;
+  const uint8_t* p11 = vox + (z1 - zb) * sz + y1 * sy;
   const R ofx = (R)1 - fx, ofy = (R)1 - fy, ofz = (R)1 - fz;
   const R c00 = (R)__ldg(p00 + x0) * ofx + (R)__ldg(p00 + x1) * fx;
   const R c10 = (R)__ldg(p10 + x0) * ofx + (R)__ldg(p10 + x1) * fx;
@@ -65,7 +71,7 @@ __device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R
 
 template <typename R>
 __device__ __forceinline__ R sample_world(const uint8_t* __restrict__ vox, R px, R py, R pz, R inv_vx, int nx, int ny,
-                                          int nz) {
+                                          int nz, int zb) {
   // render.py:114-122
   const R ux = px * inv_vx + (R)(nx - 1) * (R)0.5;
   const R uy = py * inv_vx + (R)(ny - 1) * (R)0.5;
@@ -73,7 +79,7 @@ __device__ __forceinline__ R sample_world(const uint8_t* __restrict__ vox, R px,
   if (ux < (R)-0.5 || ux > (R)nx - (R)0.5 || uy < (R)-0.5 || uy > (R)ny - (R)0.5 || uz < (R)-0.5 ||
       uz > (R)nz - (R)0.5)
     return (R)-1;
-  return sample_tri<R>(vox, ux, uy, uz, nx, ny, nz);
+  return sample_tri<R>(vox, ux, uy, uz, nx, ny, nz, zb);
 }
 
 // Conservative range of k whose sample may lie inside |p_axis| <= half (+ margin).
@@ -116,9 +122,9 @@ __device__ __forceinline__ uint8_t to_u8_unit(R v) {  // floor(min(v, 1) * 255 +
 }
 
 template <typename R>
-__global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__ vox, int nx, int ny, int nz,
-                                                     const __grid_constant__ ViewBatch views, int dim, int row0,
-                                                     int row1, uint8_t* __restrict__ out) {
+__global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__ vox, int zb, int nx, int ny,
+                                                     int nz, const __grid_constant__ ViewBatch views, int dim,
+                                                     int row0, int row1, uint8_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
   const int view = blockIdx.z;
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     R acc = 0;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
       if (v > (R)0) acc += v;
     }
     R val = (R)V.gain * acc / (R)steps;
@@ -165,12 +171,12 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     R shade = 0;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
       if (v >= thr) {
         R t_lo = t - dt, t_hi = t;
         for (int b = 0; b < 4; b++) {
           const R tm = (R)0.5 * (t_lo + t_hi);
-          const R vm = sample_world<R>(vox, rox + dx * tm, roy + dy * tm, roz, inv_vx, nx, ny, nz);
+          const R vm = sample_world<R>(vox, rox + dx * tm, roy + dy * tm, roz, inv_vx, nx, ny, nz, zb);
           if (vm >= thr) t_hi = tm;
           else t_lo = tm;
         }
@@ -179,9 +185,9 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
         const R ux = hx * inv_vx + (R)(nx - 1) * (R)0.5;
         const R uy = hy * inv_vx + (R)(ny - 1) * (R)0.5;
         const R uz = hz * inv_vx + (R)(nz - 1) * (R)0.5;
-        const R gx = sample_tri<R>(vox, ux + (R)1, uy, uz, nx, ny, nz) - sample_tri<R>(vox, ux - (R)1, uy, uz, nx, ny, nz);
-        const R gy = sample_tri<R>(vox, ux, uy + (R)1, uz, nx, ny, nz) - sample_tri<R>(vox, ux, uy - (R)1, uz, nx, ny, nz);
-        const R gz = sample_tri<R>(vox, ux, uy, uz + (R)1, nx, ny, nz) - sample_tri<R>(vox, ux, uy, uz - (R)1, nx, ny, nz);
+        const R gx = sample_tri<R>(vox, ux + (R)1, uy, uz, nx, ny, nz, zb) - sample_tri<R>(vox, ux - (R)1, uy, uz, nx, ny, nz, zb);
+        const R gy = sample_tri<R>(vox, ux, uy + (R)1, uz, nx, ny, nz, zb) - sample_tri<R>(vox, ux, uy - (R)1, uz, nx, ny, nz, zb);
+        const R gz = sample_tri<R>(vox, ux, uy, uz + (R)1, nx, ny, nz, zb) - sample_tri<R>(vox, ux, uy, uz - (R)1, nx, ny, nz, zb);
         const R gn = sqrt(gx * gx + gy * gy + gz * gz);
         if (gn < (R)1e-12) {
           shade = 1;
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     R m = 0;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
       m = v > m ? v : m;
     }
     if (m > (R)255) m = (R)255;
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     const R stop = (R)V.early_stop;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
       if (v < (R)0) continue;
       R c[4];
       tf_eval<R>(V.tf, V.slope, v, c);
@@ -248,7 +254,7 @@ __device__ __forceinline__ uint4 tld4_a2d(cudaTextureObject_t tex, int layer, fl
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex, int nx, int ny, int nz,
+__global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex, int zb, int nx, int ny, int nz,
                                                          const __grid_constant__ ViewBatch views, int dim, int row0,
                                                          int row1, uint8_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
   // per-row constants: the row's two slices and z weight (render.py:72-79, 105-111)
   const int zf = (int)floor(uzd);
   const float fz = (float)(uzd - (double)zf);
-  const int l0 = min(max(zf, 0), nz - 1), l1 = min(max(zf + 1, 0), nz - 1);
+  const int l0 = min(max(zf, 0), nz - 1) - zb, l1 = min(max(zf + 1, 0), nz - 1) - zb;  // texture layers = slab slices
   // u(k) = a + k * b exactly as an FMA per step (no drift): u = (o + d*t)*n + (n-1)/2, t = -R + (k+1/2)dt
   const double bx = G.dx * G.dt * G.inv_vx, by = G.dy * G.dt * G.inv_vx;
   const double ax = (ox + G.dx * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(nx - 1) * 0.5;
@@ -336,32 +342,95 @@ __device__ __forceinline__ float4 tld4f_a2d(cudaTextureObject_t tex, int layer, 
   return r;
 }
 
-__global__ void blend_rows_kernel(const uint8_t* __restrict__ vol, int nx, int ny, int nz, double big_r, double px_size,
-                                  double inv_vx, int row0, cudaSurfaceObject_t surf) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
+// Empty-space skipping (MIP and alpha on the row planes): the planes are cut into
+// kSkip x kSkip texel blocks and each block stores the max 8.8 value over its
+// texels DILATED by one texel on the high side -- every bilinear footprint whose
+// lower-left texel lies in the block is covered -- so a run of samples inside a
+// block whose bound is <= the running maximum (MIP) or <= the transfer
+// function's zero-alpha level (alpha) cannot change the pixel and is stepped
+// over analytically.
+constexpr int kSkip = 8;
+constexpr int kBlendCols = 256;
+
+// one CTA = kBlendCols columns x one kSkip-row band of one row plane: blends the
+// two slices into the plane (8.8 fixed point, |error| <= 1/512 of a gray level)
+// and writes the band's block maxima.
+__global__ void __launch_bounds__(kBlendCols) blend_rows_kernel(const uint8_t* __restrict__ vol, int zb, int nx, int ny, int nz,
+                                                                double big_r, double px_size, double inv_vx, int row0,
+                                                                cudaSurfaceObject_t surf, uint16_t* __restrict__ bmax,
+                                                                int nbx, int nby) {
+  __shared__ uint16_t colmax[kBlendCols + 1];
+  const int x = blockIdx.x * kBlendCols + threadIdx.x;
+  const int by = blockIdx.y;
   const int layer = blockIdx.z;
-  if (x >= nx) return;
   const int j = row0 + layer;
   const double wy = big_r - ((double)j + 0.5) * px_size;
   const double uz = wy * inv_vx + (double)(nz - 1) * 0.5;
-  float v = 0.f;
-  if (!(uz < -0.5 || uz > (double)nz - 0.5)) {
+  const bool inside = !(uz < -0.5 || uz > (double)nz - 0.5);
+  int z0 = 0, z1 = 0;
+  float fz = 0.f;
+  if (inside) {
     const int zf = (int)floor(uz);
-    const float fz = (float)(uz - (double)zf);
-    const int z0 = min(max(zf, 0), nz - 1), z1 = min(max(zf + 1, 0), nz - 1);
-    const float a = (float)__ldg(vol + ((int64_t)z0 * ny + y) * nx + x);
-    const float b = (float)__ldg(vol + ((int64_t)z1 * ny + y) * nx + x);
-    v = fmaf(fz, b - a, a);
+    fz = (float)(uz - (double)zf);
+    z0 = min(max(zf, 0), nz - 1);
+    z1 = min(max(zf + 1, 0), nz - 1);
   }
-  // 8.8 fixed point: |error| <= 1/512 of a gray level
-  surf2DLayeredwrite((unsigned short)__float2uint_rn(v * 256.0f), surf, x * (int)sizeof(unsigned short), y, layer);
+  const uint8_t* s0 = vol + (int64_t)(inside ? z0 - zb : 0) * ny * nx;  // vol holds slices [zb, ...)
+  const uint8_t* s1 = vol + (int64_t)(inside ? z1 - zb : 0) * ny * nx;
+  const int ya = by * kSkip, yw = min(ya + kSkip, ny), yd = min(ya + kSkip, ny - 1);
+  auto texel = [&](int xx, int yy) -> uint32_t {
+    if (!inside) return 0u;
+    const float a = (float)__ldg(s0 + (int64_t)yy * nx + xx), b = (float)__ldg(s1 + (int64_t)yy * nx + xx);
+    return __float2uint_rn(fmaf(fz, b - a, a) * 256.0f);
+  };
+  uint32_t cm = 0;
+  if (x < nx) {
+    for (int y = ya; y <= yd; y++) {
+      const uint32_t t = texel(x, y);
+      if (y < yw) surf2DLayeredwrite((unsigned short)t, surf, x * (int)sizeof(unsigned short), y, layer);
+      cm = max(cm, t);
+    }
+  }
+  colmax[threadIdx.x] = (uint16_t)cm;
+  if (threadIdx.x == 0) {  // the dilation column of the CTA's last block
+    const int xe = blockIdx.x * kBlendCols + kBlendCols;
+    uint32_t ce = 0;
+    if (xe < nx)
+      for (int y = ya; y <= yd; y++) ce = max(ce, texel(xe, y));
+    colmax[kBlendCols] = (uint16_t)ce;
+  }
+  __syncthreads();
+  const int bx = blockIdx.x * (kBlendCols / kSkip) + threadIdx.x;
+  if (threadIdx.x < kBlendCols / kSkip && bx < nbx) {
+    uint32_t b = 0;
+#pragma unroll
+    for (int q = 0; q <= kSkip; q++) b = max(b, (uint32_t)colmax[threadIdx.x * kSkip + q]);
+    bmax[((int64_t)layer * nby + by) * nbx + bx] = (uint16_t)b;
+  }
+}
+
+// first step index at which floor(u(k)) leaves [lo, lo + kSkip) along one axis
+// (u(k) = a + k b); conservative by construction of the caller (it re-checks one
+// step early).  Returns INT_MAX when the axis never leaves (b == 0 or open edge).
+__device__ __forceinline__ int block_exit(float a, float b, int blk, int nblk) {
+  float t;
+  if (b > 0.f) {
+    if (blk >= nblk - 1) return INT_MAX;
+    t = ((float)((blk + 1) * kSkip) - a) / b;
+  } else if (b < 0.f) {
+    if (blk <= 0) return INT_MAX;
+    t = ((float)(blk * kSkip) - a) / b;
+  } else {
+    return INT_MAX;
+  }
+  return t < 1.0e9f ? (int)ceilf(t) : INT_MAX;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t tex, int nx, int ny, int nz,
                                                           const __grid_constant__ ViewBatch views, int dim, int row0,
-                                                          int row1, uint8_t* __restrict__ out) {
+                                                          int row1, uint8_t* __restrict__ out,
+                                                          const uint16_t* __restrict__ bmax, int nbx, int nby, int skip) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
   const int view = blockIdx.z;
@@ -388,32 +457,60 @@ __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t te
   const double ay = (oy + G.dy * (-G.big_r + 0.5 * G.dt)) * G.inv_vx + (double)(ny - 1) * 0.5;
   const float fax = (float)ax, fbx = (float)bx, fay = (float)ay, fby = (float)by;
   const float xlo = -0.5f, xhi = (float)nx - 0.5f, ylo = -0.5f, yhi = (float)ny - 0.5f;
-  float m = 0.f;
+  float m = 0.f;  // MIP: running max in 8.8 units (the final * 1/256 is exact)
   float C0 = 0.f, C1 = 0.f, C2 = 0.f, A = 0.f;
-  const float stop = V.early_stop;
+  if (MODE == CTP_MODE_MIP) {
+    // MIP: every sample (a noisy background leaves no block below the running
+    // max often enough to pay for the lookups -- measured)
 #pragma unroll 4
-  for (int k = klo; k <= khi; k++) {
-    const float ux = fmaf((float)k, fbx, fax), uy = fmaf((float)k, fby, fay);
-    if (ux < xlo || ux > xhi || uy < ylo || uy > yhi) continue;
-    const float x0 = floorf(ux), y0 = floorf(uy);
-    const float fx = ux - x0, fy = uy - y0;
-    const uint4 gi = tld4_a2d(tex, layer, x0 + 1.0f, y0 + 1.0f);  // .w (x0,y0) .z (x1,y0) .x (x0,y1) .y (x1,y1)
-    const float4 g = make_float4((float)gi.x, (float)gi.y, (float)gi.z, (float)gi.w);
-    const float a0 = fmaf(fx, g.z - g.w, g.w), a1 = fmaf(fx, g.y - g.x, g.x);
-    const float v = fmaf(fy, a1 - a0, a0) * (1.0f / 256.0f);
-    if (MODE == CTP_MODE_MIP) {
-      m = fmaxf(m, v);
-    } else {
+    for (int k = klo; k <= khi; k++) {
+      const float ux = fmaf((float)k, fbx, fax), uy = fmaf((float)k, fby, fay);
+      if (ux < xlo || ux > xhi || uy < ylo || uy > yhi) continue;
+      const float x0 = floorf(ux), y0 = floorf(uy);
+      const float fx = ux - x0, fy = uy - y0;
+      const uint4 gi = tld4_a2d(tex, layer, x0 + 1.0f, y0 + 1.0f);  // .w (x0,y0) .z (x1,y0) .x (x0,y1) .y (x1,y1)
+      const float4 g = make_float4((float)gi.x, (float)gi.y, (float)gi.z, (float)gi.w);
+      const float a0 = fmaf(fx, g.z - g.w, g.w), a1 = fmaf(fx, g.y - g.x, g.x);
+      m = fmaxf(m, fmaf(fy, a1 - a0, a0));
+    }
+  } else {
+    // alpha: samples in blocks whose bound is at or below the transfer function's
+    // zero-alpha level contribute w = (1 - A) * 0 exactly and are stepped over
+    const uint16_t* bm = bmax + (int64_t)layer * nby * nbx;
+    const float stop = V.early_stop;
+    const float zero_lvl = skip ? V.skip_lvl : -1.f;
+    int cur = -1;  // block of the last bound lookup
+    float bound = 0.f;
+    int k = klo;
+    while (k <= khi) {
+      const float ux = fmaf((float)k, fbx, fax), uy = fmaf((float)k, fby, fay);
+      if (ux < xlo || ux > xhi || uy < ylo || uy > yhi) { k++; continue; }
+      const float x0 = floorf(ux), y0 = floorf(uy);
+      const int bxi = min(max((int)x0, 0) / kSkip, nbx - 1), byi = min(max((int)y0, 0) / kSkip, nby - 1);
+      const int blk = byi * nbx + bxi;
+      if (blk != cur) { cur = blk; bound = (float)__ldg(bm + blk); }
+      if (bound <= zero_lvl) {
+        // resume one step before the ray leaves the block (the re-check absorbs fp rounding)
+        const int kn = min(block_exit(fax, fbx, bxi, nbx), block_exit(fay, fby, byi, nby));
+        k = (kn == INT_MAX) ? khi + 1 : max(k + 1, kn - 1);
+        continue;
+      }
+      const float fx = ux - x0, fy = uy - y0;
+      const uint4 gi = tld4_a2d(tex, layer, x0 + 1.0f, y0 + 1.0f);
+      const float4 g = make_float4((float)gi.x, (float)gi.y, (float)gi.z, (float)gi.w);
+      const float a0 = fmaf(fx, g.z - g.w, g.w), a1 = fmaf(fx, g.y - g.x, g.x);
       float c[4];
-      tf_eval<float>(V.tf, V.slope, v, c);
+      tf_eval<float>(V.tf, V.slope, fmaf(fy, a1 - a0, a0) * (1.0f / 256.0f), c);
       const float w = (1.f - A) * c[3];
       C0 = fmaf(w, c[0], C0);
       C1 = fmaf(w, c[1], C1);
       C2 = fmaf(w, c[2], C2);
       A += w;
+      k++;
       if (A >= stop) break;
     }
   }
+  m *= (1.0f / 256.0f);
   if (MODE == CTP_MODE_MIP) {
     const uint8_t o = (uint8_t)(int)floorf(fminf(m, 255.f) + 0.5f);
     if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(o, o, o, 255);
@@ -429,12 +526,58 @@ struct RowPlanes {
   cudaArray_t arr = nullptr;
   cudaTextureObject_t tex = 0;
   cudaSurfaceObject_t surf = 0;
+  uint16_t* bmax = nullptr;  // (rows, nby, nbx) block maxima
+  int64_t rows = 0, ny = 0, nx = 0;
   ~RowPlanes() {
+    if (bmax) cudaFree(bmax);
     if (tex) cudaDestroyTextureObject(tex);
     if (surf) cudaDestroySurfaceObject(surf);
     if (arr) cudaFreeArray(arr);
   }
 };
+
+// Row planes stay allocated between calls (per device, reused while the plane
+// shape is unchanged): allocating and freeing a 2 GiB layered array costs
+// milliseconds, a 36-view batch renders in ~40 ms.  ctp_render_release() frees them.
+constexpr int kMaxDevices = 64;
+static std::mutex g_planes_mu;
+static std::unique_ptr<RowPlanes> g_planes[kMaxDevices];
+
+static int get_planes(RowPlanes** out, int64_t rows, int64_t ny, int64_t nx) {
+  int d = 0;
+  CTP_CUDA_CALL(cudaGetDevice(&d));
+  CTP_REQUIRE(d >= 0 && d < kMaxDevices, CTP_E_INVALID, "device %d out of range", d);
+  std::unique_ptr<RowPlanes>& slot = g_planes[d];
+  if (slot && slot->rows == rows && slot->ny == ny && slot->nx == nx) {
+    *out = slot.get();
+    return CTP_OK;
+  }
+  slot.reset();  // free the old shape before allocating the new one
+  std::unique_ptr<RowPlanes> rp(new RowPlanes());
+  cudaChannelFormatDesc fd = cudaCreateChannelDesc<unsigned short>();
+  CTP_CUDA_CALL(cudaMalloc3DArray(&rp->arr, &fd, make_cudaExtent((size_t)nx, (size_t)ny, (size_t)rows),
+                                  cudaArrayLayered | cudaArraySurfaceLoadStore));
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = rp->arr;
+  CTP_CUDA_CALL(cudaCreateSurfaceObject(&rp->surf, &rd));
+  cudaTextureDesc td = {};
+  td.addressMode[0] = cudaAddressModeClamp;
+  td.addressMode[1] = cudaAddressModeClamp;
+  td.addressMode[2] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  CTP_CUDA_CALL(cudaCreateTextureObject(&rp->tex, &rd, &td, nullptr));
+  const int64_t nbx = (nx + kSkip - 1) / kSkip, nby = (ny + kSkip - 1) / kSkip;
+  CTP_CUDA_CALL(cudaMalloc(&rp->bmax, (size_t)rows * nbx * nby * sizeof(uint16_t)));
+  rp->rows = rows;
+  rp->ny = ny;
+  rp->nx = nx;
+  slot = std::move(rp);
+  *out = slot.get();
+  return CTP_OK;
+}
 
 struct TexVolume {
   cudaArray_t arr = nullptr;
@@ -481,17 +624,24 @@ __global__ void image_hist_kernel(const uint8_t* __restrict__ imgs, int64_t pixe
     if (hs[b]) atomicAdd(hist + (int64_t)img * 256 + b, (unsigned long long)hs[b]);
 }
 
-}  // namespace ctp
+// Slices a row band reads, for any mode and either precision: the trilinear
+// pair around uz(j) (render.py:105-111) plus the surface gradient's +-1 and a
+// one-slice margin for the fp32 floor (render.py:185-192).
+static void row_slices(int64_t j, double big_r, double px_size, double n_max, int64_t nz, int64_t* lo, int64_t* hi) {
+  const double uz = (big_r - ((double)j + 0.5) * px_size) * n_max + (double)(nz - 1) * 0.5;
+  if (uz < -0.51 || uz > (double)nz - 0.49) { *lo = 1; *hi = 0; return; }  // row outside the volume: no slices
+  const int64_t zf = (int64_t)floor(uz);
+  *lo = zf - 2 < 0 ? 0 : zf - 2;
+  *hi = zf + 3 > nz - 1 ? nz - 1 : zf + 3;
+}
 
-using namespace ctp;
-
-extern "C" {
-
-int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const ctp_view* views, int32_t n_views,
-                  int64_t row0, int64_t row1, uint8_t* out, void* stream) {
+static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, int64_t ny, int64_t nx,
+                       const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out, void* stream) {
   CTP_REQUIRE(vol && views && out, CTP_E_INVALID, "ctp_render_u8: null pointer");
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1 && nx < (1LL << 31) && ny < (1LL << 31) && nz < (1LL << 31),
               CTP_E_INVALID, "ctp_render_u8: bad shape");
+  CTP_REQUIRE(0 <= zb && snz >= 1 && zb + snz <= nz, CTP_E_INVALID, "slab [%lld, %lld) outside [0, %lld)",
+              (long long)zb, (long long)(zb + snz), (long long)nz);
   CTP_REQUIRE(n_views >= 1 && n_views <= 65535, CTP_E_INVALID, "n_views %d outside [1, 65535]", n_views);
   const ctp_view& v0 = views[0];
   const int dim = v0.image_dim;
@@ -538,59 +688,71 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const 
         hv[q].slope[a][b] = v.fp32 ? (double)(((float)c1 - (float)c0) / ((float)x1 - (float)x0)) : (c1 - c0) / (x1 - x0);
       }
     hv[q].early_stop = v.early_stop;
+    // alpha is exactly 0 up to the last leading control point with alpha 0
+    // (flat segments between them have slope 0; tf_eval clamps below tf[0])
+    float zl = -1.f;
+    for (int a = 0; a < 4 && v.tf[a][4] == 0.f; a++) zl = v.tf[a][0] * 256.0f;
+    if (v.mode != CTP_MODE_ALPHA) zl = -1.f;
+    hv[q].skip_lvl = zl;
+  }
+  if (zb != 0 || snz != nz) {  // a z-slab: every requested row must read only held slices
+    for (int64_t j = row0; j < row1; j++) {
+      int64_t lo, hi;
+      row_slices(j, hv[0].g.big_r, hv[0].g.px_size, hv[0].g.inv_vx, nz, &lo, &hi);
+      CTP_REQUIRE(lo > hi || (lo >= zb && hi < zb + snz), CTP_E_INVALID,
+                  "row %lld reads slices [%lld, %lld], slab holds [%lld, %lld)", (long long)j, (long long)lo,
+                  (long long)hi, (long long)zb, (long long)(zb + snz));
+    }
   }
   cudaStream_t st = as_stream(stream);
   ViewBatch vb;
   for (int q = 0; q < n_views; q++) vb.v[q] = hv[q];
   dim3 grid((dim + 127) / 128, (unsigned)(row1 - row0), (unsigned)n_views);
-  const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && nz <= 2048 &&
+  const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && snz <= 2048 &&
                         nx <= 32768 && ny <= 32768;
   if (tex_path) {
     // row planes when they fit comfortably (4 B per voxel per image row)
+    std::unique_lock<std::mutex> lock(g_planes_mu);  // held until the planes' last reader finished
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
+    int dev_id = 0;
+    cudaGetDevice(&dev_id);
+    if (dev_id >= 0 && dev_id < kMaxDevices && g_planes[dev_id])  // cached planes count as free
+      free_b += (size_t)g_planes[dev_id]->rows * g_planes[dev_id]->ny * g_planes[dev_id]->nx * 2;
     const size_t plane_bytes = (size_t)(row1 - row0) * (size_t)nx * (size_t)ny * 2;
     const char* rp_env = getenv("CTP_RENDER_ROWPLANES");  // "0" forces the two-gather path
     if (!(rp_env && rp_env[0] == '0') && row1 - row0 <= 2048 && plane_bytes < free_b / 2) {
-      RowPlanes rp;
-      cudaChannelFormatDesc fd = cudaCreateChannelDesc<unsigned short>();
-      CTP_CUDA_CALL(cudaMalloc3DArray(&rp.arr, &fd, make_cudaExtent((size_t)nx, (size_t)ny, (size_t)(row1 - row0)),
-                                      cudaArrayLayered | cudaArraySurfaceLoadStore));
-      cudaResourceDesc rd = {};
-      rd.resType = cudaResourceTypeArray;
-      rd.res.array.array = rp.arr;
-      CTP_CUDA_CALL(cudaCreateSurfaceObject(&rp.surf, &rd));
-      cudaTextureDesc td = {};
-      td.addressMode[0] = cudaAddressModeClamp;
-      td.addressMode[1] = cudaAddressModeClamp;
-      td.addressMode[2] = cudaAddressModeClamp;
-      td.filterMode = cudaFilterModePoint;
-      td.readMode = cudaReadModeElementType;
-      td.normalizedCoords = 0;
-      CTP_CUDA_CALL(cudaCreateTextureObject(&rp.tex, &rd, &td, nullptr));
+      RowPlanes* rpp = nullptr;
+      int rc = get_planes(&rpp, row1 - row0, ny, nx);
+      if (rc != CTP_OK) return rc;
+      RowPlanes& rp = *rpp;
       const RenderGeom& G0 = hv[0].g;
-      dim3 bg((unsigned)((nx + 127) / 128), (unsigned)ny, (unsigned)(row1 - row0));
-      blend_rows_kernel<<<bg, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx, (int)row0,
-                                            rp.surf);
+      const char* sk_env = getenv("CTP_RENDER_SKIP");  // "0" disables empty-space skipping
+      const int skip = (sk_env && sk_env[0] == '0') ? 0 : 1;
+      const int nbx = (int)((nx + kSkip - 1) / kSkip), nby = (int)((ny + kSkip - 1) / kSkip);
+      dim3 bg((unsigned)((nx + kBlendCols - 1) / kBlendCols), (unsigned)nby, (unsigned)(row1 - row0));
+      blend_rows_kernel<<<bg, kBlendCols, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx,
+                                                   (int)row0, rp.surf, rp.bmax, nbx, nby);
       CTP_CUDA_CHECK_LAUNCH("blend_rows_kernel");
       if (v0.mode == CTP_MODE_MIP)
         render_rows_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
-                                                               (int)row1, out);
+                                                               (int)row1, out, rp.bmax, nbx, nby, skip);
       else
         render_rows_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
-                                                                 (int)row1, out);
+                                                                 (int)row1, out, rp.bmax, nbx, nby, skip);
       CTP_CUDA_CHECK_LAUNCH("render_rows_kernel");
       CTP_CUDA_CALL(cudaStreamSynchronize(st));  // planes must outlive the kernel
       return CTP_OK;
     }
+    lock.unlock();
     TexVolume tv;
-    int rc = make_tex_volume(tv, vol, nz, ny, nx, st);
+    int rc = make_tex_volume(tv, vol, snz, ny, nx, st);
     if (rc != CTP_OK) return rc;
     if (v0.mode == CTP_MODE_MIP)
-      render_tex_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(tv.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+      render_tex_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(tv.tex, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
                                                             (int)row1, out);
     else
-      render_tex_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(tv.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+      render_tex_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(tv.tex, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
                                                               (int)row1, out);
     CTP_CUDA_CHECK_LAUNCH("render_tex_kernel");
     // the array / texture object must outlive the kernel
@@ -598,10 +760,33 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const 
     return CTP_OK;
   }
   if (v0.fp32)
-    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
+    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
   else
-    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
+    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
   CTP_CUDA_CHECK_LAUNCH("render_kernel");
+  return CTP_OK;
+}
+
+}  // namespace ctp
+
+using namespace ctp;
+
+extern "C" {
+
+int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const ctp_view* views, int32_t n_views,
+                  int64_t row0, int64_t row1, uint8_t* out, void* stream) {
+  return render_impl(vol, 0, nz, nz, ny, nx, views, n_views, row0, row1, out, stream);
+}
+
+int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz, int64_t nz, int64_t ny, int64_t nx,
+                       const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out,
+                       void* stream) {
+  return render_impl(slab, z_base, slab_nz, nz, ny, nx, views, n_views, row0, row1, out, stream);
+}
+
+int ctp_render_release(void) {
+  std::lock_guard<std::mutex> lock(g_planes_mu);
+  for (int d = 0; d < kMaxDevices; d++) g_planes[d].reset();
   return CTP_OK;
 }
 

@@ -255,11 +255,16 @@ def make_view(p, channels: int = 1, fp32: bool = False) -> View:
 
 
 def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False, rows=None,
-           out: torch.Tensor | None = None) -> torch.Tensor:
+           out: torch.Tensor | None = None, z_base: int = 0, full_nz: int | None = None) -> torch.Tensor:
     """render.py:205-236, batched over views (<= 64 per launch).
-    Returns uint8 (n, rows, dim) or (n, rows, dim, 4)."""
+    Returns uint8 (n, rows, dim) or (n, rows, dim, 4).
+
+    ``vol`` may be a z-slab (slices [z_base, z_base + vol.shape[0]) of a volume
+    ``full_nz`` deep): the geometry is the full volume's and every requested row
+    must read only held slices (``dist.row_slices``), else the library refuses."""
     _check_dev(vol, torch.uint8, "render")
-    nz, ny, nx = vol.shape
+    snz, ny, nx = vol.shape
+    nz = snz if full_nz is None else int(full_nz)
     params_list = list(params_list)
     n = len(params_list)
     dim = int(params_list[0].image_dim)
@@ -270,9 +275,18 @@ def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False
     for b in range(0, n, 64):
         chunk = params_list[b:b + 64]
         arr = (View * len(chunk))(*[make_view(p, channels, fp32) for p in chunk])
-        _lib.call("ctp_render_u8", _ptr(vol), nz, ny, nx, arr, len(chunk), r0, r1, _ptr(out[b:b + len(chunk)]),
-                  _stream())
+        if z_base == 0 and snz == nz:
+            _lib.call("ctp_render_u8", _ptr(vol), nz, ny, nx, arr, len(chunk), r0, r1, _ptr(out[b:b + len(chunk)]),
+                      _stream())
+        else:
+            _lib.call("ctp_render_slab_u8", _ptr(vol), z_base, snz, nz, ny, nx, arr, len(chunk), r0, r1,
+                      _ptr(out[b:b + len(chunk)]), _stream())
     return out
+
+
+def render_release() -> None:
+    """Free the row planes the fp32 MIP/alpha path keeps between calls."""
+    _lib.call("ctp_render_release")
 
 
 def image_hist(imgs: torch.Tensor) -> torch.Tensor:

@@ -1,4 +1,5 @@
-"""z-slab sharding of one volume across the GPUs of a node.
+"""z-slab sharding of one volume across the GPUs of a node:
+the preview step (``ShardedPreview``) and sort-last rendering (``ShardedRender``).
 
 Rank r owns slices [z0_r, z1_r) with every slab height a multiple of 2^nlev,
 so no pyramid cell straddles two ranks (no halo).  One step:
@@ -17,8 +18,10 @@ product binds it to the CUDA kernels (``DeviceSlabCompute``).
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -181,3 +184,152 @@ class ShardedPreview:
                    for l, (a, b) in self.ranges(self.rank).items()]
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+
+
+# ---------------------------------------------------------------------------
+# Sort-last rendering of a z-slab-sharded volume.
+#
+# The reference camera has elevation 0 (render.py:131-140): pixel row j's rays
+# all lie in the plane z = wy(j), so row j samples only the slices around
+# uz(j).  The per-slab partial images of a sort-last renderer are therefore
+# disjoint row bands and the composite is a row-band gather: rank r renders the
+# rows whose clamped floor(uz) lies in its core slices [z0, z1), from its core
+# plus a halo of the slices those rows read (the trilinear pair, the surface
+# gradient's +-1 and one slice of margin -- ``row_slices``, the same rule the
+# library enforces in ctp_render_slab_u8).
+
+def render_geometry(shape, image_dim: int) -> tuple[float, float, float]:
+    """(big_r, px_size, n_max) of render.py:212-223 for a (nz, ny, nx) volume."""
+    nz, ny, nx = shape
+    n_max = float(max(nz, ny, nx))
+    hx, hy, hz = nx / (2.0 * n_max), ny / (2.0 * n_max), nz / (2.0 * n_max)
+    big_r = math.sqrt(hx * hx + hy * hy + hz * hz)
+    return big_r, 2.0 * big_r / image_dim, n_max
+
+
+def row_uz(shape, image_dim: int) -> np.ndarray:
+    """Voxel-space z of every image row (render.py:131-137, 114-118), fp64 in the kernel's order."""
+    nz = shape[0]
+    big_r, px, n_max = render_geometry(shape, image_dim)
+    j = np.arange(image_dim, dtype=np.float64)
+    return (big_r - (j + 0.5) * px) * n_max + (nz - 1) * 0.5
+
+
+def row_slices(shape, image_dim: int) -> tuple[np.ndarray, np.ndarray]:
+    """Per row, the inclusive slice window [lo, hi] it reads (lo > hi: none)."""
+    nz = shape[0]
+    uz = row_uz(shape, image_dim)
+    inside = (uz >= -0.51) & (uz <= nz - 0.49)
+    zf = np.floor(uz).astype(np.int64)
+    lo = np.where(inside, np.clip(zf - 2, 0, nz - 1), 1)
+    hi = np.where(inside, np.clip(zf + 3, 0, nz - 1), 0)
+    return lo, hi
+
+
+def row_band(shape, image_dim: int, z0: int, z1: int) -> tuple[int, int]:
+    """Rows whose clamped floor(uz) lies in [z0, z1): contiguous, since uz falls with j."""
+    nz = shape[0]
+    owner = np.clip(np.floor(row_uz(shape, image_dim)), 0, nz - 1).astype(np.int64)
+    rows = np.flatnonzero((owner >= z0) & (owner < z1))
+    if rows.size == 0:
+        return 0, 0
+    r0, r1 = int(rows[0]), int(rows[-1]) + 1
+    assert rows.size == r1 - r0
+    return r0, r1
+
+
+def held_slices(shape, image_dim: int, z0: int, z1: int) -> tuple[int, int]:
+    """Slices a rank must hold to render its row band: its core plus the halo the band reads."""
+    r0, r1 = row_band(shape, image_dim, z0, z1)
+    lo, hi = row_slices(shape, image_dim)
+    h0, h1 = z0, z1
+    for j in range(r0, r1):
+        if lo[j] <= hi[j]:
+            h0, h1 = min(h0, int(lo[j])), max(h1, int(hi[j]) + 1)
+    return h0, h1
+
+
+class RenderCompute:
+    """Interface of the per-rank renderer (device kernels in production)."""
+
+    def render(self, slab, z_base: int, full_nz: int, views, rows, channels: int, fp32: bool):  # pragma: no cover
+        raise NotImplementedError
+
+
+class DeviceRenderCompute(RenderCompute):
+    def __init__(self):
+        from . import device as dev
+        self.dev = dev
+
+    def render(self, slab, z_base, full_nz, views, rows, channels, fp32):
+        return self.dev.render(slab, views, channels=channels, fp32=fp32, rows=rows, z_base=z_base, full_nz=full_nz)
+
+
+@dataclass
+class ShardedRender:
+    """One rank's share of a batch of views, volume z-slab-sharded (sort-last) or
+    replicated (image rows split evenly).  ``render`` returns the full images on
+    rank 0 (``gather``) and this rank's row band everywhere else."""
+
+    shape: tuple                 # full volume (nz, ny, nx)
+    image_dim: int
+    compute: RenderCompute
+    rank: int
+    world: int
+    device: torch.device
+    replicated: bool = False
+    align: int = 1               # core slab alignment (the preview's, to share its slabs)
+    group: object = None
+
+    def __post_init__(self):
+        nz = self.shape[0]
+        self.cores, self.bands, self.held = [], [], []
+        for r in range(self.world):
+            if self.replicated:
+                d = self.image_dim
+                self.cores.append((0, nz))
+                self.bands.append((r * d // self.world, (r + 1) * d // self.world))
+                self.held.append((0, nz))
+            else:
+                z0, z1 = slab_bounds(nz, self.world, r, self.align)
+                self.cores.append((z0, z1))
+                self.bands.append(row_band(self.shape, self.image_dim, z0, z1))
+                self.held.append(held_slices(self.shape, self.image_dim, z0, z1))
+        cover = sorted(b for b in self.bands if b[1] > b[0])
+        if cover[0][0] != 0 or cover[-1][1] != self.image_dim or any(p[1] != q[0] for p, q in zip(cover, cover[1:])):
+            raise AssertionError(f"row bands {self.bands} do not partition [0, {self.image_dim})")
+        self.z0, self.z1 = self.cores[self.rank]
+        self.h0, self.h1 = self.held[self.rank]
+        self.r0, self.r1 = self.bands[self.rank]
+
+    def render(self, local: torch.Tensor, views, channels: int = 1, fp32: bool = False, gather: bool = True):
+        """local: slices [h0, h1) of the volume on ``device`` (the whole volume when replicated)."""
+        views = list(views)
+        n, d = len(views), self.image_dim
+        tail = (d,) if channels == 1 else (d, channels)
+        band = None
+        if self.r1 > self.r0:
+            band = self.compute.render(local, self.h0, self.shape[0], views, (self.r0, self.r1), channels, fp32)
+        if self.world == 1 or not gather:
+            return band
+        if self.rank == 0:
+            out = torch.empty((n, d) + tail, dtype=torch.uint8, device=self.device)
+            if band is not None:
+                out[:, self.r0:self.r1] = band
+            bufs, ops = {}, []
+            for r in range(1, self.world):
+                a, b = self.bands[r]
+                if b > a:
+                    bufs[r] = torch.empty((n, b - a) + tail, dtype=torch.uint8, device=self.device)
+                    ops.append(dist.P2POp(dist.irecv, bufs[r], r, group=self.group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            for r, t in bufs.items():
+                a, b = self.bands[r]
+                out[:, a:b] = t
+            return out
+        if band is not None:
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, band.contiguous(), 0, group=self.group)]):
+                w.wait()
+        return band

@@ -128,3 +128,89 @@ def test_slab_bounds_and_alignment():
         assert atlas_byte_range(schemes[512], z0 >> 1, z1 >> 1) == (r * 4096 * 4096, (r + 1) * 4096 * 4096)
     with pytest.raises(ValueError):
         atlas_byte_range(schemes[512], 3, 64)
+
+
+class OracleRenderCompute:
+    """Test-only RenderCompute: the CPU oracle on a volume that holds ONLY this
+    rank's slab -- every other slice is poisoned, so a row that read outside its
+    rank's held slices would differ from the whole-volume render."""
+
+    def render(self, slab, z_base, full_nz, views, rows, channels, fp32):
+        from oracle import ctp_oracle as O
+        v = slab.numpy()
+        full = np.full((full_nz,) + v.shape[1:], 251, dtype=np.uint8)
+        full[z_base:z_base + v.shape[0]] = v
+        imgs = [_oracle_image(O, full, p) for p in views]
+        return torch.from_numpy(np.stack(imgs)[:, rows[0]:rows[1]].copy())
+
+
+def _oracle_image(O, vol, p):
+    if p.mode == "mip":
+        return O.render_mip(vol, p.azimuth_deg, p.image_dim, p.steps)
+    return O.render_view(vol, p.azimuth_deg, p.image_dim, p.steps, p.mode, p.threshold)
+
+
+def _render_worker(rank, world, port, q, replicated):
+    try:
+        sys.path.insert(0, str(ROOT))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2311_15038_b200.dist import ShardedRender
+        from paper_2311_15038_b200.types import ViewParams
+        from oracle import ctp_oracle as O
+
+        rng = np.random.default_rng(7)
+        nz, ny, nx = 40, 36, 44  # non-cubic: the rows of the image cover more than the volume
+        vol = np.clip(np.rint(rng.normal(20, 6, (nz, ny, nx))), 0, 255).astype(np.uint8)
+        zz, yy, xx = np.mgrid[:nz, :ny, :nx]
+        shell = np.abs(np.sqrt(((zz - 19.5) / 15) ** 2 + ((yy - 17) / 13) ** 2 + ((xx - 22) / 17) ** 2) - 1.0) < 0.12
+        vol[shell] = 180
+        dim = 80  # rows finer than slices: the bands' edge rows need the halo (core-only slabs fail)
+        views = [ViewParams(azimuth_deg=a, image_dim=dim, steps=64, mode=m, threshold=90)
+                 for m in ("surface", "mip") for a in (0.0, 130.0)]
+        sr = ShardedRender((nz, ny, nx), dim, OracleRenderCompute(), rank, world, torch.device("cpu"),
+                           replicated=replicated)
+        local = torch.from_numpy(vol[sr.h0:sr.h1].copy())
+        out = sr.render(local, views, channels=1)
+        if rank == 0:
+            ref = np.stack([_oracle_image(O, vol, p) for p in views])
+            ok = np.array_equal(out.numpy(), ref)
+            q.put(("ok" if ok else "mismatch", (sr.bands, sr.held)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", repr(e)))
+
+
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("replicated", [False, True])
+def test_sharded_render_gloo_world2(replicated):
+    """Sort-last z-slab rendering (row-band gather) and the replicated image-row split
+    equal the whole-volume oracle images bit for bit."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_render_worker, args=(r, 2, port, q, replicated)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=230)
+    status, info = q.get(timeout=5)
+    assert status == "ok", info
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_row_bands_partition_and_halo():
+    from paper_2311_15038_b200.dist import held_slices, row_band, row_slices, slab_bounds
+
+    for shape, dim in (((1024, 1024, 1024), 1024), ((96, 80, 112), 64), ((2048, 1536, 1536), 512)):
+        lo, hi = row_slices(shape, dim)
+        for world in (1, 2, 4, 8):
+            bands = [row_band(shape, dim, *slab_bounds(shape[0], world, r, 1)) for r in range(world)]
+            rows = sorted(j for a, b in bands for j in range(a, b))
+            assert rows == list(range(dim))
+            for r, (a, b) in enumerate(bands):
+                h0, h1 = held_slices(shape, dim, *slab_bounds(shape[0], world, r, 1))
+                for j in range(a, b):
+                    assert lo[j] > hi[j] or (h0 <= lo[j] and hi[j] < h1)

@@ -433,3 +433,65 @@ def test_c4_full_size_mip_rows_vs_exact_path(P, cuda):
             assert int(d.max()) <= 1, (mode, r0, int(d.max()))
     del vol
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- z-slab (sort-last) rendering, empty-space skipping
+
+def _shell_volume(shape, seed=3):
+    rng = np.random.default_rng(seed)
+    nz, ny, nx = shape
+    vol = np.clip(np.rint(rng.normal(20, 6, shape)), 0, 255).astype(np.uint8)
+    zz, yy, xx = np.mgrid[:nz, :ny, :nx]
+    r = np.sqrt(((zz - nz / 2) / (0.4 * nz)) ** 2 + ((yy - ny / 2) / (0.35 * ny)) ** 2 + ((xx - nx / 2) / (0.4 * nx)) ** 2)
+    vol[np.abs(r - 1.0) < 0.08] = 190
+    return vol
+
+
+def test_render_slab_bands_equal_whole_volume(P, cuda):
+    """Every mode/precision: the row band rendered from a rank's slab + halo equals the
+    same rows rendered from the whole volume bit for bit (sort-last = row-band gather)."""
+    from paper_2311_15038_b200 import _lib, device as dev, dist as D
+    shape = (72, 60, 84)
+    nz = shape[0]
+    vt = torch.from_numpy(_shell_volume(shape)).to(cuda)
+    dim = 112
+    cases = [("surface", 1, False), ("additive", 1, False), ("mip", 1, False), ("mip", 4, True), ("alpha", 4, True),
+             ("alpha", 4, False)]
+    for world in (2, 3, 5):
+        for r in range(world):
+            z0, z1 = D.slab_bounds(nz, world, r, 1)
+            r0, r1 = D.row_band(shape, dim, z0, z1)
+            h0, h1 = D.held_slices(shape, dim, z0, z1)
+            if r1 <= r0:
+                continue
+            for mode, ch, fp32 in cases:
+                views = [P.ViewParams(azimuth_deg=a, image_dim=dim, steps=128, mode=mode, threshold=100, tf=TF)
+                         for a in (0.0, 123.0)]
+                whole = dev.render(vt, views, channels=ch, fp32=fp32, rows=(r0, r1)).cpu().numpy()
+                part = dev.render(vt[h0:h1].contiguous(), views, channels=ch, fp32=fp32, rows=(r0, r1), z_base=h0,
+                                  full_nz=nz).cpu().numpy()
+                assert np.array_equal(whole, part), (world, r, mode, fp32)
+    # a slab without its halo is refused, not rendered from missing slices
+    z0, z1 = D.slab_bounds(nz, 2, 0, 1)
+    r0, r1 = D.row_band(shape, dim, z0, z1)
+    views = [P.ViewParams(azimuth_deg=0.0, image_dim=dim, steps=128, mode="mip")]
+    with pytest.raises(_lib.NativeError):
+        dev.render(vt[z0:z1].contiguous(), views, channels=1, fp32=True, rows=(r0, r1), z_base=z0, full_nz=nz)
+
+
+def test_alpha_empty_space_skipping_is_exact(P, cuda, monkeypatch):
+    """fp32 alpha with block skipping (transfer function 0 below 100) equals the
+    unskipped fp32 path bit for bit and the fp64 oracle within 1/255."""
+    from paper_2311_15038_b200 import device as dev
+    vol = _shell_volume((64, 80, 96), seed=5)
+    tf = ((0.0, 0.0, 0.0, 0.0, 0.0), (100.0, 0.5, 0.3, 0.2, 0.0), (180.0, 1.0, 0.8, 0.5, 0.3),
+          (255.0, 1.0, 1.0, 1.0, 0.9))
+    vt = torch.from_numpy(vol).to(cuda)
+    views = [P.ViewParams(azimuth_deg=a, image_dim=96, steps=160, mode="alpha", tf=tf) for a in (0.0, 45.0, 200.0)]
+    skip = dev.render(vt, views, channels=4, fp32=True).cpu().numpy()
+    monkeypatch.setenv("CTP_RENDER_SKIP", "0")
+    noskip = dev.render(vt, views, channels=4, fp32=True).cpu().numpy()
+    assert np.array_equal(skip, noskip)
+    for k, p in enumerate(views):
+        ref = O.render_alpha(vol, p.azimuth_deg, 96, 160, tf, 0.99)
+        assert int(np.abs(skip[k].astype(int) - ref.astype(int)).max()) <= 1

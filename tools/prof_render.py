@@ -21,7 +21,10 @@ ap.add_argument("--dim", type=int, default=1024)
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--batches", type=int, default=1)
 ap.add_argument("--fp64", action="store_true")
+ap.add_argument("--lib", default=None, help="alternative build of the shared library (A/B timing)")
 a = ap.parse_args()
+if a.lib:
+    _lib._lib = _lib.load(a.lib)
 _lib.load()
 spec = synth.config("c4")
 if a.n != 1024:
