@@ -225,7 +225,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mip", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mip-batches", type=int, default=2)
+    ap.add_argument("--mip-batches", type=int, default=4)
     ap.add_argument("--no-configs", action="store_true", help="skip the c1 / c3 / c4-alpha side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -403,20 +403,22 @@ def main():
 
 
 def bench_mip(args, device, rank, world, dist):
-    """Config 4: 36 MIP azimuths, 1024^2 RGBA8, image-tile split across ranks (volume replicated)."""
+    """Config 4: 36 MIP azimuths, 1024^2 RGBA8.  At N > 1 the volume is z-slab
+    sharded and rendered sort-last (each rank its row band from its slab + halo,
+    bands gathered to rank 0 inside the timed region); at N = 1 the whole volume."""
     import math
     import torch
-    from paper_2311_15038_b200 import device as dev, synth
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.dist import DeviceRenderCompute, ShardedRender
     from paper_2311_15038_b200.types import ViewParams
     spec = synth.config("c4")
-    vol = synth.generate(spec, device=device)
     n = spec.shape[0]
     dim = 1024
     steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * n)  # 0.5-voxel step over the 2R window: 3548 for 1024^3
     views = [ViewParams(azimuth_deg=10.0 * k, image_dim=dim, steps=steps, mode="mip") for k in range(36)]
-    rows = (rank * dim // world, (rank + 1) * dim // world)
-    out = torch.empty((36, rows[1] - rows[0], dim, 4), dtype=torch.uint8, device=device)
-    dev.render(vol, views, channels=4, fp32=True, rows=rows, out=out)   # warmup
+    sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device)
+    local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
+    sr.render(local, views, channels=4, fp32=True)   # warmup (row planes allocated once)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -424,7 +426,7 @@ def bench_mip(args, device, rank, world, dist):
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(args.mip_batches):
-        dev.render(vol, views, channels=4, fp32=True, rows=rows, out=out)
+        sr.render(local, views, channels=4, fp32=True)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
@@ -433,14 +435,17 @@ def bench_mip(args, device, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     frames = 36 * args.mip_batches
-    del vol
+    del local
+    from paper_2311_15038_b200 import device as dev
+    dev.render_release()
     torch.cuda.empty_cache()
     return {"value": frames / (ms * 1e-3), "unit": "frames/s", "ms_per_frame": ms / frames,
             "gsamples_per_s": frames * dim * dim * steps / (ms * 1e-3) / 1e9, "steps_per_ray": steps,
             "image": "1024^2 RGBA8", "volume": "1024^3 u8 (config-4 generator)", "views_per_batch": 36,
             "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
-            "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames, image rows split across ranks"}
+            "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + (
+                "" if world == 1 else f"; z-slab x{world} sort-last: row bands from slab + halo, gathered to rank 0")}
 
 
 def _time_steps(fn, reps: int, warmup: int = 2):
