@@ -27,6 +27,7 @@ BINDINGS = {
     "optimal_snapshot": ["render", "pipeline", "cli", ""],
     "build_data_preview": ["pipeline", ""],
     "apply_circle_mask": ["mask", "pipeline", "cli", ""],
+    "build_interactive_preview": ["pipeline", ""],
 }
 
 _saved: dict = {}
@@ -45,7 +46,10 @@ def install(package: str = "ctprev") -> list[str]:
     FACTORY.SlicemapSet = sm.SlicemapSet
     FACTORY.EntropyResult = rd.EntropyResult
     FACTORY.SnapshotResult = rd.SnapshotResult
-    FACTORY.DataPreview = importlib.import_module(f"{package}.pipeline").DataPreview
+    pl = importlib.import_module(f"{package}.pipeline")
+    FACTORY.DataPreview = pl.DataPreview
+    FACTORY.InteractivePreview = pl.InteractivePreview
+    FACTORY.Circle = importlib.import_module(f"{package}.mask").Circle
     patched = []
     for name, mods in BINDINGS.items():
         new = getattr(ops, name)

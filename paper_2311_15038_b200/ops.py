@@ -337,3 +337,69 @@ def apply_circle_mask(volume, circle, margin: float = 0.02):
     r_eff = circle.r * (1.0 - margin)                                        # mask.py:208
     out = dev.circle_mask(to_device(vox), circle.cx, circle.cy, r_eff ** 2)
     return FACTORY.Volume(_host(out), getattr(volume, "voxel_size_um", None))
+
+
+def _host_helper(module: str, name: str):
+    """A host-side reference function that is not on the device path (circle
+    Hough transform, Otsu sweep): taken from the installed ctprev."""
+    try:
+        import importlib
+        return getattr(importlib.import_module(f"ctprev.{module}"), name)
+    except Exception as e:  # pragma: no cover - depends on the environment
+        raise RuntimeError(f"build_interactive_preview: ctprev.{module}.{name} (host, off the device path) is not "
+                           f"importable; pass it explicitly") from e
+
+
+def build_interactive_preview(volume, detect=None, threshold=None, margin: float = 0.02):
+    """pipeline.py:267-309 with the volume resident on the device.
+
+    Each scheme's level comes straight from full resolution (``_scheme_volume``,
+    pipeline.py:215-223); the container circle is found once on the 512-scheme
+    level's top slice by the HOST detector (``detect``, default
+    ctprev.mask.detect_container_circle -- one 2-D slice, scipy) and rescaled per
+    scheme (pipeline.py:260-264); then per scheme on the device: circle mask
+    (mask.py:194-212), 256-bin histogram, zero-padded atlases (pipeline.py:226-237);
+    the host ``threshold`` (default ctprev.threshold.otsu_threshold) reads the
+    histogram.  Only the top slice and the 256-bin histograms cross PCIe before
+    the atlases come back."""
+    from .errors import DegenerateHistogram, NoCircleFound
+    from .types import INTERACTIVE_SCHEMES, STAGES_INTERACTIVE
+    detect = detect or _host_helper("mask", "detect_container_circle")
+    threshold = threshold or _host_helper("threshold", "otsu_threshold")
+    vox = _voxels(volume)
+    nz, ny, nx = vox.shape
+    t = to_device(vox)
+    downs = {}
+    for s in INTERACTIVE_SCHEMES:
+        target = (min(s, nx), min(s, ny), min(s, nz))                            # pipeline.py:221-222
+        downs[s] = t if target == (nx, ny, nz) else _downscale_dev(t, target)
+    warnings_: list[str] = []
+    circle = None
+    try:
+        circle = detect(_host(downs[512][-1]))                                   # Volume.top_slice (volume.py:92-95)
+    except NoCircleFound:
+        warnings_.append("no_container_circle")
+    slicemaps, thresholds = {}, {}
+    for s in INTERACTIVE_SCHEMES:
+        down = downs[s]
+        if circle is not None:
+            ref = downs[512]
+            fx, fy = down.shape[2] / ref.shape[2], down.shape[1] / ref.shape[1]  # _rescale_circle, pipeline.py:260-264
+            c = FACTORY.Circle(circle.cx * fx, circle.cy * fy, circle.r * min(fx, fy), circle.votes)
+            if not (0 <= c.cx < down.shape[2] and 0 <= c.cy < down.shape[1]):   # mask.py:202-205
+                from .errors import CircleOutOfBounds
+                raise CircleOutOfBounds(f"center ({c.cx:.1f}, {c.cy:.1f}) outside {down.shape[2]}x{down.shape[1]} slice")
+            down = dev.circle_mask(down, c.cx, c.cy, (c.r * (1.0 - margin)) ** 2)
+        hist = FACTORY.Histogram256(_host(dev.hist_u8(down)))
+        try:
+            thresholds[s] = threshold(hist).value
+        except DegenerateHistogram:
+            if "degenerate_histogram" not in warnings_:
+                warnings_.append("degenerate_histogram")
+            thresholds[s] = None
+        scheme = plan_scheme(s)
+        spec = AtlasSpec.of(scheme)
+        a = _host(dev.encode_atlas(down, spec))                                  # pipeline.py:298 (+ _pad_to_cube)
+        slicemaps[s] = FACTORY.SlicemapSet(scheme=scheme, atlases=tuple(a[m] for m in range(spec.map_count)))
+    return FACTORY.InteractivePreview(slicemaps=slicemaps, circle=circle, thresholds=thresholds,
+                                      warnings=tuple(warnings_), stages=STAGES_INTERACTIVE)

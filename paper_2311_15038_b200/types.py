@@ -7,6 +7,8 @@
   ViewParams      ctprev/render.py:39-65 (+ the MIP / alpha extension modes)
   EntropyResult   ctprev/render.py:239-245
   SnapshotResult  ctprev/render.py:265-270
+  Circle          ctprev/mask.py:35-56
+  DataPreview / InteractivePreview   ctprev/pipeline.py:116-133
 
 The drop-in functions accept the reference's own objects (duck typed on the
 same attributes) and build their results through ``FACTORY``, which
@@ -19,7 +21,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import (DimensionMismatch, ManifestMismatch, RangeOutOfBounds, UnsupportedPixelFormat,
+from .errors import (CircleOutOfBounds, DimensionMismatch, ManifestMismatch, RangeOutOfBounds, UnsupportedPixelFormat,
                      UnsupportedScheme, IndexOutOfRange)
 
 SURFACE = "surface"
@@ -237,6 +239,40 @@ class DataPreview:
     stages: tuple
 
 
+STAGES_INTERACTIVE = ("slicemaps_conversion", "thresholding_container_removal")  # pipeline.py:83
+INTERACTIVE_SCHEMES = (128, 256, 512)                                          # pipeline.py:85
+
+
+@dataclass(frozen=True)
+class InteractivePreview:
+    """pipeline.py:125-133."""
+
+    slicemaps: dict
+    circle: object
+    thresholds: dict
+    warnings: tuple
+    stages: tuple
+
+
+@dataclass(frozen=True)
+class Circle:
+    """mask.py:35-56: a container circle in pixel coordinates."""
+
+    cx: float
+    cy: float
+    r: float
+    votes: float = 1.0
+
+    def __post_init__(self) -> None:
+        if self.r <= 0:
+            raise CircleOutOfBounds(f"radius {self.r} must be positive")
+        if not 0.0 <= self.votes <= 1.0:
+            raise RangeOutOfBounds(f"votes {self.votes} outside [0, 1]")
+
+    def scaled(self, factor: float) -> "Circle":
+        return type(self)(self.cx * factor, self.cy * factor, self.r * factor, self.votes)
+
+
 class _Factory:
     """Where result objects come from (switched by ``install()``)."""
 
@@ -251,6 +287,8 @@ class _Factory:
         self.EntropyResult = EntropyResult
         self.SnapshotResult = SnapshotResult
         self.DataPreview = DataPreview
+        self.InteractivePreview = InteractivePreview
+        self.Circle = Circle
 
 
 FACTORY = _Factory()

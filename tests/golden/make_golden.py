@@ -5,7 +5,8 @@ Run in the builder container, where /root/reference exists:
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
         python tests/golden/make_golden.py
 
-Writes tests/golden/ref_golden.npz and ref_golden_datapreview.npz (committed).  The GPU box never reads
+Writes tests/golden/ref_golden.npz, ref_golden_datapreview.npz and
+ref_golden_interactive.npz (committed).  The GPU box never reads
 /root/reference: tests compare the CPU oracle and the CUDA path against these
 frozen reference outputs.
 """
@@ -189,7 +190,51 @@ def data_preview_golden() -> None:
     print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
 
 
+def interactive_preview_golden() -> None:
+    """Reference build_interactive_preview (pipeline.py:267-309) on the two data-preview
+    phantoms (inputs: ref_golden_datapreview.npz dp0_in / dp1_in) and a constant
+    volume (no circle, degenerate histogram).  Stored: the circle, thresholds,
+    warnings, each scheme's masked-level histogram (recomputed with the reference's
+    own functions, the Otsu input), SHA-256 of each scheme's atlas bytes, and the
+    128-scheme atlas itself."""
+    import hashlib
+    from ctprev.mask import apply_circle_mask
+    from ctprev.pipeline import _rescale_circle, _scheme_volume, build_interactive_preview
+    from ctprev.threshold import otsu_threshold
+    dp = np.load(Path(__file__).resolve().parent / "ref_golden_datapreview.npz")
+    out = Path(__file__).resolve().parent / "ref_golden_interactive.npz"
+    const = np.full((32, 48, 40), 7, dtype=np.uint8)
+    vols = [dp["dp0_in"], dp["dp1_in"], const]
+    g = {"ip_const_in": const, "ip_n": np.array(len(vols))}
+    for i, v in enumerate(vols):
+        vol = Volume(v)
+        ip = build_interactive_preview(vol)
+        c = ip.circle
+        g[f"ip{i}_circle"] = np.array([np.nan] * 4 if c is None else [c.cx, c.cy, c.r, c.votes])
+        g[f"ip{i}_warnings"] = np.array(",".join(ip.warnings))
+        for s in (128, 256, 512):
+            t = ip.thresholds[s]
+            g[f"ip{i}_thr{s}"] = np.array(-1 if t is None else t)
+            a = np.stack(ip.slicemaps[s].atlases)
+            g[f"ip{i}_sha{s}"] = np.array(hashlib.sha256(a.tobytes()).hexdigest())
+            g[f"ip{i}_shape{s}"] = np.array(a.shape)
+            down = _scheme_volume(vol, s)
+            if c is not None:
+                down = apply_circle_mask(down, _rescale_circle(c, _scheme_volume(vol, 512), down))
+            h = volume_histogram(down)
+            g[f"ip{i}_hist{s}"] = h.bins.copy()
+            if t is not None:
+                assert otsu_threshold(h).value == t
+        g[f"ip{i}_atlas128"] = np.stack(ip.slicemaps[128].atlases)
+    np.savez_compressed(out, **g)
+    print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
+
+
 if __name__ == "__main__":
+    if "--only-interactive" in sys.argv:
+        interactive_preview_golden()
+        sys.exit(0)
     if "--only-extra" not in sys.argv:
         main()
     data_preview_golden()
+    interactive_preview_golden()

@@ -495,3 +495,47 @@ def test_alpha_empty_space_skipping_is_exact(P, cuda, monkeypatch):
     for k, p in enumerate(views):
         ref = O.render_alpha(vol, p.azimuth_deg, 96, 160, tf, 0.99)
         assert int(np.abs(skip[k].astype(int) - ref.astype(int)).max()) <= 1
+
+
+def test_build_interactive_preview_golden(P, golden_dp):
+    """pipeline.py:267-309 on the device vs the reference on two mounted phantoms and a
+    constant volume: masked-level histograms (the Otsu input) bit-exact, thresholds,
+    warnings, and every scheme's atlas bytes (SHA-256; the 128 scheme byte for byte).
+    The host-side circle detector and Otsu sweep are injected (the reference's circle,
+    the oracle's pinned Otsu restatement) -- neither is on the device path."""
+    import hashlib
+    from pathlib import Path
+    from paper_2311_15038_b200 import ops
+    from paper_2311_15038_b200.errors import DegenerateHistogram, NoCircleFound
+    from paper_2311_15038_b200.types import Circle
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_interactive.npz") as z:
+        g = {k: z[k] for k in z.files}
+    vols = [golden_dp["dp0_in"], golden_dp["dp1_in"], g["ip_const_in"]]
+    for i, v in enumerate(vols):
+        c = g[f"ip{i}_circle"]
+
+        def detect(top, c=c):
+            assert top.shape == v.shape[1:]
+            if np.isnan(c[0]):
+                raise NoCircleFound("golden: no circle")
+            return Circle(*[float(x) for x in c])
+
+        seen = []
+
+        def otsu(h):
+            seen.append(np.asarray(h.bins).copy())
+            t = O.otsu_threshold(h.bins)
+            if t is None:
+                raise DegenerateHistogram("all histogram mass in a single bin")
+            return type("R", (), {"value": t})()
+
+        ip = ops.build_interactive_preview(P.Volume(v), detect=detect, threshold=otsu)
+        assert ",".join(ip.warnings) == str(g[f"ip{i}_warnings"]), i
+        for k, s in enumerate((128, 256, 512)):
+            assert np.array_equal(seen[k], g[f"ip{i}_hist{s}"]), (i, s)
+            t = ip.thresholds[s]
+            assert (-1 if t is None else t) == int(g[f"ip{i}_thr{s}"]), (i, s)
+            a = np.stack(ip.slicemaps[s].atlases)
+            assert a.shape == tuple(g[f"ip{i}_shape{s}"]), (i, s)
+            assert hashlib.sha256(a.tobytes()).hexdigest() == str(g[f"ip{i}_sha{s}"]), (i, s)
+        assert np.array_equal(np.stack(ip.slicemaps[128].atlases), g[f"ip{i}_atlas128"]), i

@@ -199,3 +199,14 @@ def test_circle_mask_golden():
     for i in range(int(g["cm_n"])):
         cx, cy, r, m = g[f"cm{i}_params"]
         assert np.array_equal(O.apply_circle_mask(g["cm_in"], cx, cy, r, m), g[f"cm{i}_out"]), i
+
+
+def test_otsu_matches_reference_interactive_golden():
+    """The oracle's Otsu sweep reproduces the reference thresholds of
+    build_interactive_preview from the same (reference-computed) histograms."""
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_interactive.npz")
+    for i in range(int(g["ip_n"])):
+        for s in (128, 256, 512):
+            t = O.otsu_threshold(g[f"ip{i}_hist{s}"])
+            assert (-1 if t is None else t) == int(g[f"ip{i}_thr{s}"]), (i, s)
