@@ -9,15 +9,18 @@
  * as a maintainer would bind them from ctprev.
  *
  * Conventions
- *   - All pointers are DEVICE pointers unless the name ends in _host.
+ *   - Data pointers are DEVICE pointers (view/level descriptor arrays are host).
  *   - Volumes are C-contiguous (nz, ny, nx), x fastest (volume.py:38-62).
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
  *     Calls are asynchronous on that stream; nothing here synchronises
- *     except the *_host entry points, which return with results ready.
+ *     except the fp32 MIP / alpha render paths, which wait for their kernels
+ *     (the texture objects they bind must outlive them).
  *   - Return value: CTP_OK (0) or a negative CTP_E* code; the message of the
  *     last failure on the calling thread is ctp_last_error().  Nothing
- *     throws across the ABI.  No global mutable state: functions are
- *     re-entrant ("pure and re-entrant").
+ *     throws across the ABI.  Functions are re-entrant ("pure and
+ *     re-entrant"); the one piece of state kept between calls is the fp32
+ *     render path's per-device row-plane cache (mutex-guarded,
+ *     ctp_render_release() frees it).
  */
 #ifndef CTPREV_B200_H
 #define CTPREV_B200_H
