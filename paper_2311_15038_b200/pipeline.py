@@ -175,14 +175,56 @@ class PreviewSession:
         assert host_vol.shape == self.shape and host_vol.dtype == self.dtype
         if not self.streaming:
             return self._run_whole(host_vol)
+        return self._stream(lambda z0, z1, slot: host_vol[z0:z1], lambda slot, evt: None)
+
+    def run_reader(self, read) -> dict:
+        """Volume from a reader instead of host memory: ``read(z0, z1, out)`` fills the
+        pinned numpy array ``out`` (z1 - z0, ny, nx) with slices [z0, z1) (e.g. straight
+        from a .raw file).  Reading chunk c+1 overlaps chunk c's copy and pass; only
+        ``ring`` chunks of host memory are ever held."""
+        nz, ny, nx = self.shape
+        if not self.streaming:
+            full = torch.empty(self.shape, dtype=self.dtype, pin_memory=True)
+            read(0, nz, full.numpy())
+            return self._run_whole(full)
+        if not hasattr(self, "host_ring"):
+            self.host_ring = [torch.empty((self.chunk, ny, nx), dtype=self.dtype, pin_memory=True)
+                              for _ in range(len(self.ring))]
+            self.host_top = torch.empty((self.n_top, ny, nx), dtype=self.dtype, pin_memory=True)
+        freed = [None] * len(self.host_ring)
+        top_freed = getattr(self, "_top_freed", None)
+        if top_freed is not None:
+            top_freed.synchronize()  # the previous run's top-slab H2D is done
+
+        def src(z0, z1, slot):
+            if slot < 0:  # the top slab
+                read(z0, z1, self.host_top.numpy())
+                return self.host_top
+            if freed[slot] is not None:
+                freed[slot].synchronize()  # the previous H2D out of this host slot is done
+            v = self.host_ring[slot][: z1 - z0]
+            read(z0, z1, v.numpy())
+            return v
+
+        def done(slot, evt):
+            if slot >= 0:
+                freed[slot] = evt
+            else:
+                self._top_freed = evt
+
+        return self._stream(src, done)
+
+    def _stream(self, src, h2d_done) -> dict:
         nz, ny, nx = self.shape
         cur = torch.cuda.current_stream(self.device)
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             s.wait_stream(cur)
         with torch.cuda.stream(self.s_h2d):
-            self.top.copy_(host_vol[nz - self.n_top:], non_blocking=True)
+            top_src = src(nz - self.n_top, nz, -1)
+            self.top.copy_(top_src, non_blocking=True)
             top_ready = torch.cuda.Event()
             top_ready.record(self.s_h2d)
+        h2d_done(-1, top_ready)
         with torch.cuda.stream(self.s_cmp):
             self.s_cmp.wait_event(top_ready)
             lut, flags = dev.artifact_lut_fused(self.top, self.n_top, self.frac, zero_hist=self.hist)
@@ -193,12 +235,14 @@ class PreviewSession:
             z1 = min(nz, z0 + self.chunk)
             slot = c % len(self.ring)
             buf = self.ring[slot][: z1 - z0]
+            host = src(z0, z1, slot)
             with torch.cuda.stream(self.s_h2d):
                 if free[slot] is not None:
                     self.s_h2d.wait_event(free[slot])
-                buf.copy_(host_vol[z0:z1], non_blocking=True)
+                buf.copy_(host, non_blocking=True)
                 landed = torch.cuda.Event()
                 landed.record(self.s_h2d)
+            h2d_done(slot, landed)
             with torch.cuda.stream(self.s_cmp):
                 self.s_cmp.wait_event(landed)
                 outs = {l: self.atlases[s] for s, l in self.plan.scheme_level.items()}

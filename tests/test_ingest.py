@@ -1,0 +1,136 @@
+"""Ingest: ctprev's raw + JSON header format streamed into the
+device path.  Header validation and the chunk reader run on the CPU; the
+streamed preview is compared with the in-memory one on the GPU."""
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+REF = Path("/root/reference/pkg/src")
+
+
+def _write(tmp, name, vol, header=None):
+    nz, ny, nx = vol.shape
+    (tmp / f"{name}.raw").write_bytes(vol.tobytes())
+    h = {"dims": [nx, ny, nz], "dtype": "u8", "order": "xyz", "voxel_size_um": 1.5} if header is None else header
+    (tmp / f"{name}.json").write_text(h if isinstance(h, str) else json.dumps(h))
+    return tmp / f"{name}.json"
+
+
+def _bad_headers(tmp):
+    vol = np.arange(2 * 3 * 4, dtype=np.uint8).reshape(2, 3, 4)
+    cases = {
+        "json": _write(tmp, "json", vol, "{not json"),
+        "dtype": _write(tmp, "dtype", vol, {"dims": [4, 3, 2], "dtype": "u16", "order": "xyz"}),
+        "order": _write(tmp, "order", vol, {"dims": [4, 3, 2], "dtype": "u8", "order": "zyx"}),
+        "dims": _write(tmp, "dims", vol, {"dims": [4, 3], "dtype": "u8", "order": "xyz"}),
+        "size": _write(tmp, "size", vol, {"dims": [4, 3, 3], "dtype": "u8", "order": "xyz"}),
+    }
+    _write(tmp, "missing", vol)
+    (tmp / "missing.raw").unlink()
+    cases["missing"] = tmp / "missing.json"
+    return cases
+
+
+def test_read_header_errors(tmp_path):
+    from paper_2311_15038_b200 import errors as E
+    from paper_2311_15038_b200.ingest import read_header
+    want = {"json": E.InvalidManifest, "dtype": E.UnsupportedPixelFormat, "order": E.UnsupportedPixelFormat,
+            "dims": E.InvalidManifest, "size": E.DimensionMismatch, "missing": E.MissingSlice}
+    for k, p in _bad_headers(tmp_path).items():
+        with pytest.raises(want[k]):
+            read_header(p)
+    vol = np.zeros((5, 6, 7), dtype=np.uint8)
+    shape, raw, vs = read_header(_write(tmp_path, "ok", vol))
+    assert shape == (5, 6, 7) and raw.name == "ok.raw" and vs == 1.5
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not mounted")
+def test_read_header_errors_match_load_volume(tmp_path):
+    """Same error class NAMES and messages as the reference's load_volume (volume.py:229-249)."""
+    import subprocess
+    import sys
+    cases = _bad_headers(tmp_path)
+    code = ("import sys, json; sys.path.insert(0, %r)\n"
+            "from ctprev.volume import load_volume\n"
+            "out = {}\n"
+            "for k, p in json.loads(sys.argv[1]).items():\n"
+            "    try:\n        load_volume(p); out[k] = None\n"
+            "    except Exception as e:\n        out[k] = [type(e).__name__, str(e)]\n"
+            "print(json.dumps(out))\n") % str(REF)
+    r = subprocess.run([sys.executable, "-c", code, json.dumps({k: str(p) for k, p in cases.items()})],
+                       capture_output=True, text=True, env={"NUMBA_CACHE_DIR": "/tmp/numba_cache_ingest",
+                                                            "PYTHONDONTWRITEBYTECODE": "1", "PATH": "/usr/bin"})
+    ref = json.loads(r.stdout.strip().splitlines()[-1])
+    from paper_2311_15038_b200.ingest import read_header
+    for k, p in cases.items():
+        try:
+            read_header(p)
+            got = None
+        except Exception as e:
+            got = [type(e).__name__, str(e)]
+        if k == "json":  # the JSON decoder's own message text
+            assert got[0] == ref[k][0]
+        else:
+            assert got == ref[k], k
+
+
+def test_raw_reader_slabs(tmp_path):
+    from paper_2311_15038_b200.ingest import RawReader, read_header
+    rng = np.random.default_rng(3)
+    vol = rng.integers(0, 256, size=(37, 19, 23), dtype=np.uint8)
+    shape, raw, _ = read_header(_write(tmp_path, "v", vol))
+    with RawReader(raw, shape) as rd:
+        for z0, z1 in ((0, 37), (34, 37), (5, 17), (36, 37)):
+            out = np.empty((z1 - z0,) + shape[1:], dtype=np.uint8)
+            rd(z0, z1, out)
+            assert np.array_equal(out, vol[z0:z1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,schemes,chunk", [((256, 256, 256), (256, 128), 32), ((200, 200, 200), (128,), 64)])
+def test_preview_from_raw_equals_in_memory(tmp_path, cuda, shape, schemes, chunk):
+    """Streamed from disk through pinned chunks == preview_pipeline on the loaded volume
+    (power-of-two levels stream in z-chunks; a general ratio runs whole-volume)."""
+    import paper_2311_15038_b200 as P
+    from paper_2311_15038_b200.ingest import preview_from_raw
+    rng = np.random.default_rng(11)
+    vol = np.clip(np.rint(rng.normal(20, 6, shape)), 0, 255).astype(np.uint8)
+    vol[shape[0] // 3: shape[0] // 2, 40:120, 30:150] = rng.integers(120, 220, size=(shape[0] // 2 - shape[0] // 3, 80, 120),
+                                                                     dtype=np.uint8)
+    vol[-3:] = rng.integers(0, 60, size=(3,) + shape[1:], dtype=np.uint8)
+    hp = _write(tmp_path, "scan", vol)
+    got = preview_from_raw(hp, schemes=schemes, chunk_slices=chunk)
+    ref = P.preview_pipeline(P.Volume(vol), schemes=schemes)
+    assert np.array_equal(got.histogram, ref.histogram)
+    assert got.bins == ref.bins
+    for s in schemes:
+        assert np.array_equal(np.stack(got.slicemaps[s].atlases), np.stack(ref.slicemaps[s].atlases)), s
+
+
+@pytest.mark.gpu
+def test_preview_session_host_buffers_equal_in_memory(cuda):
+    """PreviewSession.run (pinned host volume -> z-chunk H2D / fused pass / atlas D2H on
+    three streams, the bench's e2e path) == the one-launch device step, twice in a row
+    (buffers reused)."""
+    import torch
+    import paper_2311_15038_b200 as P
+    from paper_2311_15038_b200.device import AtlasSpec
+    from paper_2311_15038_b200.pipeline import PreviewSession
+    rng = np.random.default_rng(5)
+    shape = (512, 256, 256)
+    schemes = {256: AtlasSpec.of(P.plan_scheme(256)), 128: AtlasSpec.of(P.plan_scheme(128))}
+    sess = PreviewSession(shape, torch.uint8, schemes, chunk_slices=64)
+    for it in range(2):
+        vol = np.clip(np.rint(rng.normal(30 + 10 * it, 8, shape)), 0, 255).astype(np.uint8)
+        vol[-3:, :64] = 200
+        host = torch.from_numpy(vol).pin_memory()
+        out = sess.run(host)
+        ref = P.preview_pipeline(P.Volume(vol), schemes=(256, 128))
+        assert np.array_equal(out["hist"].numpy(), ref.histogram)
+        assert frozenset(np.nonzero(out["flags"].numpy())[0].tolist()) == ref.bins
+        for s in (256, 128):
+            assert np.array_equal(out["atlases"][s].numpy(), np.stack(ref.slicemaps[s].atlases)), (it, s)
