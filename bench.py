@@ -566,6 +566,33 @@ def bench_other_configs(device):
                                         "overlapped with H2D + fused pass, atlases back to host (session reused)",
                             "ms_per_volume": min(ts) * 1e3, "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9,
                             "host_bytes_held": 3 * 64 * ny * nx + 3 * ny * nx}
+    # atlas PNG writing: the c2 step's 14 atlases (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2)
+    # as save_slicemaps writes them -- device filter + parallel deflate vs Pillow (slicemap.py:164)
+    import io
+    from PIL import Image
+    from paper_2311_15038_b200.png import encode_pngs
+    vol = synth.generate(spec, device=device)
+    schemes = {s: AtlasSpec.of(plan_scheme(s)) for s in (512, 256, 128)}
+    res = run_preview(vol, plan_preview(spec.shape, schemes))
+    del vol
+    host = {s: res.atlases[s].cpu().numpy() for s in schemes}
+    encode_pngs(res.atlases[128])  # warm-up
+    t0 = time.perf_counter()
+    ours = sum(len(b) for b in encode_pngs([res.atlases[s] for s in schemes]))
+    t_ours = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pil = 0
+    for s in schemes:
+        for a in host[s]:
+            buf = io.BytesIO()
+            Image.fromarray(a, mode="L").save(buf, format="PNG")
+            pil += buf.tell()
+    t_pil = time.perf_counter() - t0
+    out["c2_png"] = {"workload": "c2 atlases to PNG bytes (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2): device scanline "
+                                 "filter + parallel zlib-6 deflate blocks vs Pillow single-threaded (slicemap.py:164)",
+                     "ms": t_ours * 1e3, "bytes": ours, "pillow_ms": t_pil * 1e3, "pillow_bytes": pil,
+                     "host_threads": os.cpu_count()}
+    del res
     torch.cuda.empty_cache()
     return out
 

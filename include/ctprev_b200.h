@@ -224,6 +224,17 @@ int ctp_render_release(void);
 int ctp_image_hist_u8(const uint8_t* imgs, int32_t n_images, int64_t pixels,
                       uint64_t* hist, void* stream);
 
+/* ---------------- atlas PNG encoding --------------- */
+
+/* PNG scanline filtering for save_slicemaps (slicemap.py:158-166, which
+ * writes every atlas with Pillow): for each row of n_images grayscale
+ * images (height x width, u8) picks the PNG filter (None/Sub/Up/Average/
+ * Paeth, bpp 1) with the smallest sum of |signed residual| (ties: lowest
+ * type) and writes [filter byte, residuals] -- out is
+ * n_images x height x (width + 1) bytes, the raw stream a PNG IDAT deflates. */
+int ctp_png_filter_u8(const uint8_t* images, int32_t n_images, int64_t height, int64_t width,
+                      uint8_t* out, void* stream);
+
 /* ---------------- synthetic inputs (BASELINE configs) ------------------- */
 
 /* One ellipsoidal shell of the synthetic generators. */

@@ -5,7 +5,8 @@ The public surface mirrors the reference's hot-path API
 
     volume_histogram, Histogram256.of, artifact_bins, filter_histogram_bins,
     downscale_volume, encode_slicemaps, decode_slicemaps, plan_scheme,
-    slice_cell, render_view, image_entropy, optimal_snapshot
+    slice_cell, render_view, image_entropy, optimal_snapshot, apply_circle_mask,
+    build_data_preview, build_interactive_preview, save_slicemaps
 
 plus the fused one-pass ``preview_pipeline`` and batched ``render_views``
 (MIP / front-to-back alpha extensions).  All arithmetic runs in the sm_100a
@@ -16,7 +17,8 @@ no CPU fallback.  ``install()`` rebinds these functions inside an imported
 from .errors import *  # noqa: F401,F403
 from .types import (ADDITIVE, ALPHA, MIP, SURFACE, EntropyResult, Histogram256, SlicemapScheme, SlicemapSet,
                     SnapshotResult, ViewParams, Volume, plan_scheme, slice_cell)
-from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, decode_slicemaps, downscale_volume, encode_slicemaps,
+from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, build_interactive_preview,
+                  decode_slicemaps, downscale_volume, encode_slicemaps, save_slicemaps,
                   filter_histogram_bins, image_entropy, optimal_snapshot, preview_pipeline, render_view,
                   render_views, volume_histogram)
 from .install import install, uninstall
@@ -28,5 +30,6 @@ __all__ = [
     "SnapshotResult", "SURFACE", "ADDITIVE", "MIP", "ALPHA", "plan_scheme", "slice_cell",
     "volume_histogram", "artifact_bins", "filter_histogram_bins", "downscale_volume", "encode_slicemaps",
     "decode_slicemaps", "render_view", "render_views", "image_entropy", "optimal_snapshot",
-    "preview_pipeline", "PreviewResult", "build_data_preview", "apply_circle_mask", "install", "uninstall",
+    "preview_pipeline", "PreviewResult", "build_data_preview", "build_interactive_preview", "apply_circle_mask",
+    "save_slicemaps", "install", "uninstall",
 ]

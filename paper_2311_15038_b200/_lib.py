@@ -91,6 +91,7 @@ SIGNATURES = {
     "ctp_render_u8": [_P, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
     "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
     "ctp_render_release": [],
+    "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _P, _P],
     "ctp_image_hist_u8": [_P, _I32, _I64, _P, _P],
     "ctp_synth_volume": [_P, _I32, _I64, _I64, _I64, _I64, _I64, C.c_uint64, C.c_float, C.c_float, _I32,
                          C.POINTER(Shell), _I32, C.c_float, _P],

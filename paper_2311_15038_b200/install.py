@@ -28,6 +28,7 @@ BINDINGS = {
     "build_data_preview": ["pipeline", ""],
     "apply_circle_mask": ["mask", "pipeline", "cli", ""],
     "build_interactive_preview": ["pipeline", ""],
+    "save_slicemaps": ["slicemap", "pipeline", ""],
 }
 
 _saved: dict = {}

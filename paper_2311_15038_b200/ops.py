@@ -403,3 +403,6 @@ def build_interactive_preview(volume, detect=None, threshold=None, margin: float
         slicemaps[s] = FACTORY.SlicemapSet(scheme=scheme, atlases=tuple(a[m] for m in range(spec.map_count)))
     return FACTORY.InteractivePreview(slicemaps=slicemaps, circle=circle, thresholds=thresholds,
                                       warnings=tuple(warnings_), stages=STAGES_INTERACTIVE)
+
+
+from .png import save_slicemaps  # noqa: E402,F401  (slicemap.py:158-166, device filter + parallel deflate)

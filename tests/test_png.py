@@ -1,0 +1,97 @@
+"""Atlas PNG writing: the device scanline filter against the
+oracle restatement, the parallel-deflate PNG container against Pillow (lossless
+round trip), and save_slicemaps' files + manifest against the reference's."""
+from __future__ import annotations
+
+import io
+import json
+
+import numpy as np
+import pytest
+
+from oracle import ctp_oracle as O
+
+
+def _images():
+    rng = np.random.default_rng(8)
+    smooth = np.clip(np.cumsum(rng.integers(-3, 4, size=(3, 70, 93)), axis=2) + 128, 0, 255).astype(np.uint8)
+    noise = rng.integers(0, 256, size=(3, 70, 93), dtype=np.uint8)
+    flat = np.zeros((3, 70, 93), dtype=np.uint8)
+    flat[:, 20:40, 10:50] = 77
+    return np.concatenate([smooth, noise, flat])
+
+
+def _png_filter_unfilter_roundtrip(filt):
+    """Undo PNG filters (spec semantics) -- independent of the encoder under test."""
+    h, w1 = filt.shape
+    w = w1 - 1
+    out = np.zeros((h, w), dtype=np.int64)
+    for y in range(h):
+        f = int(filt[y, 0])
+        r = filt[y, 1:].astype(np.int64)
+        b = out[y - 1] if y > 0 else np.zeros(w, dtype=np.int64)
+        row = np.zeros(w, dtype=np.int64)
+        for x in range(w):
+            a = row[x - 1] if x > 0 else 0
+            c = b[x - 1] if x > 0 else 0
+            if f == 0:
+                pr = 0
+            elif f == 1:
+                pr = a
+            elif f == 2:
+                pr = b[x]
+            elif f == 3:
+                pr = (a + b[x]) >> 1
+            else:
+                p = a + b[x] - c
+                pa, pb, pc = abs(p - a), abs(p - b[x]), abs(p - c)
+                pr = a if (pa <= pb and pa <= pc) else (b[x] if pb <= pc else c)
+            row[x] = (r[x] + pr) & 0xFF
+        out[y] = row
+    return out.astype(np.uint8)
+
+
+def test_oracle_png_filter_inverts():
+    for img in _images()[::3]:
+        f = O.png_filter(img)
+        assert f.shape == (img.shape[0], img.shape[1] + 1) and set(np.unique(f[:, 0])) <= set(range(5))
+        assert np.array_equal(_png_filter_unfilter_roundtrip(f), img)
+
+
+def test_png_container_decodes_with_pillow():
+    from PIL import Image
+    from paper_2311_15038_b200.png import png_from_filtered
+    for img in _images():
+        for rows in (1, 7, 256):
+            data = png_from_filtered(O.png_filter(img), level=6, block_rows=rows)
+            with Image.open(io.BytesIO(data)) as im:
+                assert im.mode == "L" and im.size == (img.shape[1], img.shape[0])
+                assert np.array_equal(np.asarray(im), img)
+
+
+@pytest.mark.gpu
+def test_device_png_filter_equals_oracle(cuda):
+    import torch
+    from paper_2311_15038_b200 import device as dev
+    imgs = _images()
+    got = dev.png_filter(torch.from_numpy(imgs).to(cuda)).cpu().numpy()
+    for i in range(imgs.shape[0]):
+        assert np.array_equal(got[i], O.png_filter(imgs[i])), i
+
+
+@pytest.mark.gpu
+def test_save_slicemaps_roundtrip(cuda, tmp_path):
+    """save_slicemaps: the reference's file names and manifest; every atlas decodes
+    (Pillow, as load_slicemaps does) to the same bytes -- c1-sized 4096^2 atlas."""
+    from PIL import Image
+    import paper_2311_15038_b200 as P
+    from paper_2311_15038_b200.png import save_slicemaps
+    rng = np.random.default_rng(2)
+    vol = np.clip(np.rint(rng.normal(20, 6, (256, 256, 256))), 0, 255).astype(np.uint8)
+    vol[100:160, 60:200, 80:180] = 170
+    sset = P.encode_slicemaps(P.Volume(vol), P.SlicemapScheme(256, 4096, 16, 1))
+    mp = save_slicemaps(sset, tmp_path / "sm")
+    man = json.loads(mp.read_text())
+    assert man == {"scheme": {"s": 256, "atlas": 4096, "grid": 16, "maps": 1}, "atlases": ["sm_256_0.png"]}
+    with Image.open(tmp_path / "sm" / "sm_256_0.png") as im:
+        assert im.mode == "L" and np.array_equal(np.asarray(im), sset.atlases[0])
