@@ -13,8 +13,9 @@ ONE cooperative launch (artifact-LUT phase, grid barrier, fused pass).
 Multi-GPU (torchrun, --gpus N): the SAME 1024^3 volume is split into N z-slabs
 (strong scaling; slab heights are whole 2^3 cells and whole atlas cell rows,
 so no halo): the artifact LUT is broadcast from the rank holding the top
-slices, histograms are all-reduced (NCCL) and every rank's atlas byte range
-is gathered to rank 0 inside the step (paper_2311_15038_b200/dist.py).
+slices, histograms are all-reduced (NCCL), and every rank's fused pass stores
+its atlas cell rows straight into rank 0's atlases through a CUDA IPC mapping
+over NVLink -- the gather is part of the pass (paper_2311_15038_b200/dist.py).
 
 ``--impl reference``: the reference's CPU algorithm (the numpy oracle port of
 ctprev) on the box's host cores, process pool over z-slabs, bounded sample.
@@ -255,8 +256,9 @@ def main():
     plan = plan_preview(spec.shape, schemes)
     assert not plan.general and plan.nlev == 3
     level_of = dict(plan.scheme_level)
+    # N > 1: the atlas gather is fused into the pass (ranks > 0 store into rank 0's atlases over NVLink)
     sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), rank, world,
-                        device)
+                        device, peer_atlases=True)
     slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)  # this rank's z-slab
     stream = torch.cuda.current_stream()
     k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]

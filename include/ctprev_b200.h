@@ -235,6 +235,20 @@ int ctp_image_hist_u8(const uint8_t* imgs, int32_t n_images, int64_t pixels,
 int ctp_png_filter_u8(const uint8_t* images, int32_t n_images, int64_t height, int64_t width,
                       uint8_t* out, void* stream);
 
+/* ---------------- peer memory between the ranks of a node (s8(e)) ------- */
+
+#define CTP_IPC_HANDLE_BYTES 64
+
+/* Export a device buffer to the other processes of the node: the CUDA IPC
+ * handle of the allocation holding `ptr` and ptr's offset in it.  With the
+ * imported pointer as a level's destination, a rank's fused pass
+ * (ctp_preview_u8/u16) stores its slab's atlas rows straight into rank 0's
+ * atlases over NVLink -- the atlas gather of the z-slab sharding
+ * fused into the pass. */
+int ctp_ipc_export(const void* ptr, uint8_t* handle, int64_t* offset);
+int ctp_ipc_import(const uint8_t* handle, int64_t offset, void** ptr);
+int ctp_ipc_close(void* ptr, int64_t offset);
+
 /* ---------------- synthetic inputs (BASELINE configs) ------------------- */
 
 /* One ellipsoidal shell of the synthetic generators. */

@@ -22,7 +22,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
 # render.cu: the fp64 path must not contract a*b+c into FMA, so that its
 # arithmetic matches numba's fastmath-free reference bit for bit.
 PER_FILE = {"render.cu": ["--fmad=false"]}
-SOURCES = ["ctp_common.cu", "hist.cu", "preview.cu", "resample.cu", "render.cu", "synth.cu", "png.cu"]
+SOURCES = ["ctp_common.cu", "hist.cu", "preview.cu", "resample.cu", "render.cu", "synth.cu", "png.cu", "ipc.cu"]
 
 
 def _nvcc() -> str:

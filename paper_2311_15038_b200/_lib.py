@@ -92,6 +92,9 @@ SIGNATURES = {
     "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
     "ctp_render_release": [],
     "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _P, _P],
+    "ctp_ipc_export": [_P, _P, C.POINTER(C.c_int64)],
+    "ctp_ipc_import": [_P, _I64, C.POINTER(C.c_void_p)],
+    "ctp_ipc_close": [_P, _I64],
     "ctp_image_hist_u8": [_P, _I32, _I64, _P, _P],
     "ctp_synth_volume": [_P, _I32, _I64, _I64, _I64, _I64, _I64, C.c_uint64, C.c_float, C.c_float, _I32,
                          C.POINTER(Shell), _I32, C.c_float, _P],

@@ -62,6 +62,44 @@ def atlas_byte_range(spec: AtlasSpec, k0: int, k1: int) -> tuple[int, int]:
     return off(k0), end
 
 
+class PeerBuffer:
+    """A device buffer of another process of the node, mapped through CUDA IPC
+    (``ctp_ipc_import``); usable wherever the kernels take a destination pointer."""
+
+    def __init__(self, handle: bytes, offset: int, shape, dtype=torch.uint8):
+        import ctypes as C
+        from . import _lib
+        self._lib = _lib
+        self.offset = int(offset)
+        self.shape = tuple(shape)
+        self.dtype = dtype
+        p = C.c_void_p()
+        _lib.call("ctp_ipc_import", C.create_string_buffer(bytes(handle), len(handle)), self.offset, C.byref(p))
+        self.ptr = int(p.value)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def numel(self) -> int:
+        return int(np.prod(self.shape))
+
+    def close(self) -> None:
+        import ctypes as C
+        if self.ptr:
+            self._lib.call("ctp_ipc_close", C.c_void_p(self.ptr), self.offset)
+            self.ptr = 0
+
+
+def export_buffer(t: torch.Tensor) -> tuple[bytes, int]:
+    """(IPC handle, offset) of a CUDA tensor's storage for ``PeerBuffer`` in another process."""
+    import ctypes as C
+    from . import _lib
+    h = C.create_string_buffer(64)
+    off = C.c_int64()
+    _lib.call("ctp_ipc_export", C.c_void_p(t.data_ptr()), h, C.byref(off))
+    return h.raw, int(off.value)
+
+
 class SlabCompute:
     """Interface of the per-rank compute (device kernels in production)."""
 
@@ -108,6 +146,7 @@ class ShardedPreview:
     n_top: int = 3
     frac: float = 0.0005
     group: object = None
+    peer_atlases: bool = False   # ranks > 0 store straight into rank 0's atlases (CUDA IPC over NVLink)
 
     def __post_init__(self):
         self.fused_events = None  # optional (start, end) CUDA events around the fused pass (bench)
@@ -122,10 +161,24 @@ class ShardedPreview:
             raise ValueError("the last slab must hold the n_top top slices")
         self.hist = torch.zeros(self.compute.nbins, dtype=torch.int64, device=self.device)
         self.atlases = {}
+        self.peer = self.peer_atlases and self.world > 1
         for s, l in self.level_of.items():
             spec = self.schemes[s]
+            if self.peer and self.rank != 0:
+                continue
             self.atlases[l] = torch.zeros((spec.map_count, spec.atlas_dim, spec.atlas_dim), dtype=torch.uint8,
                                           device=self.device)
+        if self.peer:
+            # the gather fused into the pass: rank 0 exports its atlases, every other rank maps
+            # them and its kernel stores its slab's cell rows there directly (no gather step)
+            torch.cuda.synchronize(self.device)
+            handles = [{l: export_buffer(t) for l, t in self.atlases.items()} if self.rank == 0 else None]
+            dist.broadcast_object_list(handles, src=0, group=self.group)
+            if self.rank != 0:
+                for s, l in self.level_of.items():
+                    spec = self.schemes[s]
+                    h, off = handles[0][l]
+                    self.atlases[l] = PeerBuffer(h, off, (spec.map_count, spec.atlas_dim, spec.atlas_dim))
 
     def ranges(self, rank: int) -> dict:
         z0, z1 = slab_bounds(self.shape[0], self.world, rank, self.align)
@@ -166,10 +219,17 @@ class ShardedPreview:
         if self.fused_events is not None:
             self.fused_events[1].record()
         if self.world > 1:
+            # stream-ordered after every rank's pass: when rank 0's all-reduce completes, every
+            # rank's kernel -- and, in peer mode, its stores into rank 0's atlases -- is done
             dist.all_reduce(self.hist, group=self.group)
-            if gather:
+            if gather and not self.peer:
                 self._gather()
         return {"hist": self.hist, "lut": lut, "atlases": self.atlases}
+
+    def close(self) -> None:
+        for t in self.atlases.values():
+            if isinstance(t, PeerBuffer):
+                t.close()
 
     def _gather(self) -> None:
         if self.rank == 0:

@@ -1,0 +1,79 @@
+"""The atlas gather fused into the pass: in peer mode every
+rank > 0 maps rank 0's atlases through CUDA IPC and its fused kernel stores its
+slab's cell rows there directly.  Two processes on ONE GPU (gloo for the host
+collectives): the kernels never wait on one another -- each runs to completion
+on its own, the gloo all-reduce orders them -- so this is a functional test of
+the IPC path, not a timing one.  Rank 0's atlases must equal the single-process
+step bit for bit."""
+from __future__ import annotations
+
+import os
+import socket
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    try:
+        sys.path.insert(0, str(ROOT))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        device = torch.device("cuda", 0)
+        from paper_2311_15038_b200 import _lib, device as dev, synth
+        from paper_2311_15038_b200.device import AtlasSpec
+        from paper_2311_15038_b200.dist import DeviceSlabCompute, ShardedPreview
+        from paper_2311_15038_b200.types import plan_scheme
+        _lib.load()
+        spec = synth.small((256, 256, 256), seed=3)
+        schemes = {128: AtlasSpec.of(plan_scheme(128)), 64: AtlasSpec(64, 512, 8, 1)}
+        level_of = {128: 1, 64: 2}
+        fused = {1: schemes[128], 2: schemes[64]}
+        sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, fused), rank, world,
+                            device, peer_atlases=True)
+        slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)
+        res = sh.step(slab)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            full = synth.generate(spec, device=device)
+            outs, hist, _, _ = dev.preview_step(full, fused, 3, 0.0005)
+            torch.cuda.synchronize()
+            ok = torch.equal(res["hist"], hist)
+            ok &= torch.equal(res["atlases"][1], outs[1]) and torch.equal(res["atlases"][2], outs[2])
+            q.put(("ok" if ok else "mismatch", (sh.z0, sh.z1)))
+        dist.barrier()
+        sh.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", f"rank {rank}: {e!r}"))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_peer_atlases_two_processes_one_gpu(cuda):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=280)
+    status, info = q.get(timeout=5)
+    assert status == "ok", info
+    assert all(p.exitcode == 0 for p in procs)
