@@ -418,7 +418,7 @@ def bench_mip(args, device, rank, world, dist):
     dim = 1024
     steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * n)  # 0.5-voxel step over the 2R window: 3548 for 1024^3
     views = [ViewParams(azimuth_deg=10.0 * k, image_dim=dim, steps=steps, mode="mip") for k in range(36)]
-    sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device)
+    sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
     local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
     sr.render(local, views, channels=4, fp32=True)   # warmup (row planes allocated once)
     torch.cuda.synchronize()
@@ -447,7 +447,8 @@ def bench_mip(args, device, rank, world, dist):
             "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + (
-                "" if world == 1 else f"; z-slab x{world} sort-last: row bands from slab + halo, gathered to rank 0")}
+                "" if world == 1 else f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's "
+                                      "images over NVLink by the render kernels")}
 
 
 def _time_steps(fn, reps: int, warmup: int = 2):

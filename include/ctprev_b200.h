@@ -209,11 +209,14 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx,
  * [z_base, z_base + slab_nz) of an nz-deep volume; the geometry is the full
  * volume's.  Every row in [row0, row1) must read only held slices (the
  * trilinear pair, the surface gradient's +-1 and one slice of margin:
- * [floor(uz)-2, floor(uz)+3]), else CTP_E_INVALID. */
+ * [floor(uz)-2, floor(uz)+3]), else CTP_E_INVALID.  View q's band is written
+ * at out + q * out_view_stride (0 = packed bands); with `out` pointing at row
+ * row0 of a full-image buffer (stride = image bytes) -- e.g. rank 0's images
+ * mapped through ctp_ipc_import -- the sort-last composite is the render. */
 int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz,
                        int64_t nz, int64_t ny, int64_t nx,
                        const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1,
-                       uint8_t* out, void* stream);
+                       uint8_t* out, int64_t out_view_stride, void* stream);
 
 /* The fp32 MIP/alpha path keeps its per-row planes (2 B per voxel per image
  * row) allocated between calls while the shape is unchanged; this frees them. */

@@ -89,7 +89,7 @@ SIGNATURES = {
     "ctp_decode_atlas_u8": [_P, _I32, _I32, _I32, _I32, _P, _P],
     "ctp_circle_mask_u8": [_P, _I64, _I64, _I64, C.c_double, C.c_double, C.c_double, _P, _P],
     "ctp_render_u8": [_P, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
-    "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
+    "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _I64, _P],
     "ctp_render_release": [],
     "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _P, _P],
     "ctp_ipc_export": [_P, _P, C.POINTER(C.c_int64)],

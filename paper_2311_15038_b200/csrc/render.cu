@@ -41,6 +41,7 @@ struct ViewDev {
 constexpr int kMaxViews = 64;
 struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per launch
   ViewDev v[kMaxViews];
+  int64_t vstride;  // bytes between consecutive views' first rows in `out`
 };
 
 template <typename R>
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
   const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
   const int ch = V.channels;
-  uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
+  uint8_t* dst = out + (int64_t)view * views.vstride + ((int64_t)(j - row0) * dim + i) * ch;
 
   // render.py:131-137 (fp64, reference order)
   const double wy = G.big_r - ((double)j + 0.5) * G.px_size;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
   const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
   const int ch = V.channels;
-  uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
+  uint8_t* dst = out + (int64_t)view * views.vstride + ((int64_t)(j - row0) * dim + i) * ch;
   const double wy = G.big_r - ((double)j + 0.5) * G.px_size;
   const double wx = -G.big_r + ((double)i + 0.5) * G.px_size;
   const double ox = G.rx * wx, oy = G.ry * wx, oz = wy;
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t te
   const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
   const int ch = V.channels;
-  uint8_t* dst = out + (((int64_t)view * (row1 - row0) + (j - row0)) * dim + i) * ch;
+  uint8_t* dst = out + (int64_t)view * views.vstride + ((int64_t)(j - row0) * dim + i) * ch;
   const double wy = G.big_r - ((double)j + 0.5) * G.px_size;
   const double wx = -G.big_r + ((double)i + 0.5) * G.px_size;
   const double ox = G.rx * wx, oy = G.ry * wx, oz = wy;
@@ -632,7 +633,8 @@ static void row_slices(int64_t j, double big_r, double px_size, double n_max, in
 }
 
 static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, int64_t ny, int64_t nx,
-                       const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out, void* stream) {
+                       const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out,
+                       int64_t vstride, void* stream) {
   CTP_REQUIRE(vol && views && out, CTP_E_INVALID, "ctp_render_u8: null pointer");
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1 && nx < (1LL << 31) && ny < (1LL << 31) && nz < (1LL << 31),
               CTP_E_INVALID, "ctp_render_u8: bad shape");
@@ -703,6 +705,10 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
   cudaStream_t st = as_stream(stream);
   ViewBatch vb;
   for (int q = 0; q < n_views; q++) vb.v[q] = hv[q];
+  const int64_t band = (row1 - row0) * (int64_t)dim * v0.channels;
+  CTP_REQUIRE(vstride == 0 || vstride >= band, CTP_E_INVALID, "out_view_stride %lld below one band (%lld bytes)",
+              (long long)vstride, (long long)band);
+  vb.vstride = vstride ? vstride : band;
   dim3 grid((dim + 127) / 128, (unsigned)(row1 - row0), (unsigned)n_views);
   const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && snz <= 2048 &&
                         nx <= 32768 && ny <= 32768;
@@ -771,13 +777,13 @@ extern "C" {
 
 int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const ctp_view* views, int32_t n_views,
                   int64_t row0, int64_t row1, uint8_t* out, void* stream) {
-  return render_impl(vol, 0, nz, nz, ny, nx, views, n_views, row0, row1, out, stream);
+  return render_impl(vol, 0, nz, nz, ny, nx, views, n_views, row0, row1, out, 0, stream);
 }
 
 int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz, int64_t nz, int64_t ny, int64_t nx,
                        const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out,
-                       void* stream) {
-  return render_impl(slab, z_base, slab_nz, nz, ny, nx, views, n_views, row0, row1, out, stream);
+                       int64_t out_view_stride, void* stream) {
+  return render_impl(slab, z_base, slab_nz, nz, ny, nx, views, n_views, row0, row1, out, out_view_stride, stream);
 }
 
 int ctp_render_release(void) {

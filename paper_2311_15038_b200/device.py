@@ -255,13 +255,16 @@ def make_view(p, channels: int = 1, fp32: bool = False) -> View:
 
 
 def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False, rows=None,
-           out: torch.Tensor | None = None, z_base: int = 0, full_nz: int | None = None) -> torch.Tensor:
+           out: torch.Tensor | None = None, z_base: int = 0, full_nz: int | None = None,
+           out_ptr: int | None = None, out_view_stride: int = 0) -> torch.Tensor | None:
     """render.py:205-236, batched over views (<= 64 per launch).
     Returns uint8 (n, rows, dim) or (n, rows, dim, 4).
 
     ``vol`` may be a z-slab (slices [z_base, z_base + vol.shape[0]) of a volume
     ``full_nz`` deep): the geometry is the full volume's and every requested row
-    must read only held slices (``dist.row_slices``), else the library refuses."""
+    must read only held slices (``dist.row_slices``), else the library refuses.
+    ``out_ptr`` / ``out_view_stride``: write view q's band at out_ptr + q * stride
+    instead (e.g. into rank 0's full images through a peer mapping); returns None."""
     _check_dev(vol, torch.uint8, "render")
     snz, ny, nx = vol.shape
     nz = snz if full_nz is None else int(full_nz)
@@ -269,19 +272,24 @@ def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False
     n = len(params_list)
     dim = int(params_list[0].image_dim)
     r0, r1 = (0, dim) if rows is None else rows
-    shape = (n, r1 - r0, dim) if channels == 1 else (n, r1 - r0, dim, channels)
-    if out is None:
-        out = torch.empty(shape, dtype=torch.uint8, device=vol.device)
+    band = (r1 - r0) * dim * channels
+    if out_ptr is None:
+        shape = (n, r1 - r0, dim) if channels == 1 else (n, r1 - r0, dim, channels)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.uint8, device=vol.device)
+        base, stride = out.data_ptr(), band
+    else:
+        base, stride = int(out_ptr), int(out_view_stride or band)
     for b in range(0, n, 64):
         chunk = params_list[b:b + 64]
         arr = (View * len(chunk))(*[make_view(p, channels, fp32) for p in chunk])
-        if z_base == 0 and snz == nz:
-            _lib.call("ctp_render_u8", _ptr(vol), nz, ny, nx, arr, len(chunk), r0, r1, _ptr(out[b:b + len(chunk)]),
-                      _stream())
+        dst = C.c_void_p(base + b * stride)
+        if z_base == 0 and snz == nz and stride == band:
+            _lib.call("ctp_render_u8", _ptr(vol), nz, ny, nx, arr, len(chunk), r0, r1, dst, _stream())
         else:
-            _lib.call("ctp_render_slab_u8", _ptr(vol), z_base, snz, nz, ny, nx, arr, len(chunk), r0, r1,
-                      _ptr(out[b:b + len(chunk)]), _stream())
-    return out
+            _lib.call("ctp_render_slab_u8", _ptr(vol), z_base, snz, nz, ny, nx, arr, len(chunk), r0, r1, dst,
+                      stride, _stream())
+    return out if out_ptr is None else None
 
 
 def render_release() -> None:

@@ -324,6 +324,12 @@ class DeviceRenderCompute(RenderCompute):
     def render(self, slab, z_base, full_nz, views, rows, channels, fp32):
         return self.dev.render(slab, views, channels=channels, fp32=fp32, rows=rows, z_base=z_base, full_nz=full_nz)
 
+    def render_into(self, slab, z_base, full_nz, views, rows, channels, fp32, out_ptr: int, view_stride: int):
+        """Write each view's row band straight into full images at ``out_ptr`` (row 0 of view 0)."""
+        d = int(views[0].image_dim)
+        self.dev.render(slab, views, channels=channels, fp32=fp32, rows=rows, z_base=z_base, full_nz=full_nz,
+                        out_ptr=out_ptr + rows[0] * d * channels, out_view_stride=view_stride)
+
 
 @dataclass
 class ShardedRender:
@@ -340,9 +346,11 @@ class ShardedRender:
     replicated: bool = False
     align: int = 1               # core slab alignment (the preview's, to share its slabs)
     group: object = None
+    peer_images: bool = False    # ranks render their bands straight into rank 0's images (CUDA IPC)
 
     def __post_init__(self):
         nz = self.shape[0]
+        self._peer_out = {}
         self.cores, self.bands, self.held = [], [], []
         for r in range(self.world):
             if self.replicated:
@@ -362,11 +370,39 @@ class ShardedRender:
         self.h0, self.h1 = self.held[self.rank]
         self.r0, self.r1 = self.bands[self.rank]
 
+    def _peer_images(self, n: int, channels: int):
+        """Rank 0's (n, dim, dim[, ch]) image buffer, mapped on every rank (set up once per shape)."""
+        key = (n, channels)
+        if key not in self._peer_out:
+            d = self.image_dim
+            shape = (n, d, d) if channels == 1 else (n, d, d, channels)
+            buf = torch.empty(shape, dtype=torch.uint8, device=self.device) if self.rank == 0 else None
+            handle = [export_buffer(buf) if self.rank == 0 else None]
+            dist.broadcast_object_list(handle, src=0, group=self.group)
+            self._peer_out[key] = buf if self.rank == 0 else PeerBuffer(handle[0][0], handle[0][1], shape)
+        return self._peer_out[key]
+
+    def close(self) -> None:
+        for t in self._peer_out.values():
+            if isinstance(t, PeerBuffer):
+                t.close()
+        self._peer_out.clear()
+
     def render(self, local: torch.Tensor, views, channels: int = 1, fp32: bool = False, gather: bool = True):
         """local: slices [h0, h1) of the volume on ``device`` (the whole volume when replicated)."""
         views = list(views)
         n, d = len(views), self.image_dim
         tail = (d,) if channels == 1 else (d, channels)
+        if self.peer_images and self.world > 1 and gather:
+            # sort-last composite fused into the render: every rank's kernel stores its row band
+            # into rank 0's images over NVLink; the all-reduce after it (stream order) completes it
+            out = self._peer_images(n, channels)
+            if self.r1 > self.r0:
+                self.compute.render_into(local, self.h0, self.shape[0], views, (self.r0, self.r1), channels, fp32,
+                                         out.data_ptr(), d * d * channels)
+            flag = torch.ones(1, dtype=torch.int32, device=self.device)
+            dist.all_reduce(flag, group=self.group)
+            return out if self.rank == 0 else None
         band = None
         if self.r1 > self.r0:
             band = self.compute.render(local, self.h0, self.shape[0], views, (self.r0, self.r1), channels, fp32)

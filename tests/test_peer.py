@@ -62,6 +62,65 @@ def _worker(rank, world, port, q):
         q.put(("error", f"rank {rank}: {e!r}"))
 
 
+def _render_worker(rank, world, port, q):
+    try:
+        sys.path.insert(0, str(ROOT))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import math
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        device = torch.device("cuda", 0)
+        from paper_2311_15038_b200 import _lib, device as dev, synth
+        from paper_2311_15038_b200.dist import DeviceRenderCompute, ShardedRender
+        from paper_2311_15038_b200.types import ViewParams
+        _lib.load()
+        spec = synth.small((192, 160, 176), seed=4)
+        dim = 200
+        views = [ViewParams(azimuth_deg=a, image_dim=dim, steps=math.ceil(4 * math.sqrt(3) / 2 * 192), mode=m)
+                 for m in ("mip",) for a in (0.0, 70.0, 200.0)]
+        sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
+        local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
+        out = sr.render(local, views, channels=4, fp32=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            full = synth.generate(spec, device=device)
+            ref = dev.render(full, views, channels=4, fp32=True)
+            torch.cuda.synchronize()
+            q.put(("ok" if torch.equal(out, ref) else "mismatch", (sr.bands, sr.held)))
+        dist.barrier()
+        sr.close()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put(("error", f"rank {rank}: {e!r}"))
+
+
+def _run_two(target):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=280)
+    status, info = q.get(timeout=5)
+    assert status == "ok", info
+    assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_peer_images_sort_last_two_processes_one_gpu(cuda):
+    """Sort-last rendering with the composite fused into the render: each rank's kernel
+    writes its row band of every view into rank 0's images through an IPC mapping."""
+    _run_two(_render_worker)
+
+
 @pytest.mark.gpu
 @pytest.mark.timeout(300)
 def test_peer_atlases_two_processes_one_gpu(cuda):
