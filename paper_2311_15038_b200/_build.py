@@ -19,6 +19,7 @@ OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libctprev_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+COMMON += os.environ.get("CTP_NVCC_EXTRA", "").split()  # variant experiments (tools/), e.g. -DCTP_U16_COLS=8
 # render.cu: the fp64 path must not contract a*b+c into FMA, so that its
 # arithmetic matches numba's fastmath-free reference bit for bit.
 PER_FILE = {"render.cu": ["--fmad=false"]}

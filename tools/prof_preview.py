@@ -21,7 +21,10 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--config", default="c2")
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--schemes", default="512,256,128")
+ap.add_argument("--lib", default=None, help="alternative build of the shared library (A/B timing)")
 a = ap.parse_args()
+if a.lib:
+    _lib._lib = _lib.load(a.lib)
 _lib.load()
 spec = synth.config(a.config)
 vol = synth.generate(spec)
