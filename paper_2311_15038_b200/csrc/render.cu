@@ -347,17 +347,17 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
 // block whose bound is <= the transfer function's zero-alpha level contributes
 // w = (1 - A) * 0 exactly and is stepped over analytically.
 constexpr int kSkip = 8;
-constexpr int kBlendCols = 256;
+constexpr int kBlendThreads = 256, kBlendVec = 4, kBlendCols = kBlendThreads * kBlendVec;
 
 // one CTA = kBlendCols columns x one kSkip-row band of one row plane: blends the
 // two slices into the plane (8.8 fixed point, |error| <= 1/512 of a gray level)
 // and writes the band's block maxima.
-__global__ void __launch_bounds__(kBlendCols) blend_rows_kernel(const uint8_t* __restrict__ vol, int zb, int nx, int ny, int nz,
-                                                                double big_r, double px_size, double inv_vx, int row0,
-                                                                cudaSurfaceObject_t surf, uint16_t* __restrict__ bmax,
-                                                                int nbx, int nby) {
+__global__ void __launch_bounds__(kBlendThreads) blend_rows_kernel(const uint8_t* __restrict__ vol, int zb, int nx,
+                                                                   int ny, int nz, double big_r, double px_size,
+                                                                   double inv_vx, int row0, cudaSurfaceObject_t surf,
+                                                                   uint16_t* __restrict__ bmax, int nbx, int nby) {
   __shared__ uint16_t colmax[kBlendCols + 1];
-  const int x = blockIdx.x * kBlendCols + threadIdx.x;
+  const int x = blockIdx.x * kBlendCols + threadIdx.x * kBlendVec;
   const int by = blockIdx.y;
   const int layer = blockIdx.z;
   const int j = row0 + layer;
@@ -375,20 +375,44 @@ __global__ void __launch_bounds__(kBlendCols) blend_rows_kernel(const uint8_t* _
   const uint8_t* s0 = vol + (int64_t)(inside ? z0 - zb : 0) * ny * nx;  // vol holds slices [zb, ...)
   const uint8_t* s1 = vol + (int64_t)(inside ? z1 - zb : 0) * ny * nx;
   const int ya = by * kSkip, yw = min(ya + kSkip, ny), yd = min(ya + kSkip, ny - 1);
+  auto blend = [&](uint32_t a, uint32_t b) -> uint32_t {
+    return __float2uint_rn(fmaf(fz, (float)b - (float)a, (float)a) * 256.0f);
+  };
   auto texel = [&](int xx, int yy) -> uint32_t {
     if (!inside) return 0u;
-    const float a = (float)__ldg(s0 + (int64_t)yy * nx + xx), b = (float)__ldg(s1 + (int64_t)yy * nx + xx);
-    return __float2uint_rn(fmaf(fz, b - a, a) * 256.0f);
+    return blend(__ldg(s0 + (int64_t)yy * nx + xx), __ldg(s1 + (int64_t)yy * nx + xx));
   };
-  uint32_t cm = 0;
+  // 4 consecutive texels per thread: one 4-byte load per slice, one 8-byte surface store
+  const bool vec = ((nx & 3) == 0) && (x + kBlendVec <= nx);
+  uint32_t cm[kBlendVec] = {0, 0, 0, 0};
   if (x < nx) {
     for (int y = ya; y <= yd; y++) {
-      const uint32_t t = texel(x, y);
-      if (y < yw) surf2DLayeredwrite((unsigned short)t, surf, x * (int)sizeof(unsigned short), y, layer);
-      cm = max(cm, t);
+      uint32_t t[kBlendVec] = {0, 0, 0, 0};
+      if (vec) {
+        if (inside) {
+          const uint32_t a4 = __ldg(reinterpret_cast<const uint32_t*>(s0 + (int64_t)y * nx + x));
+          const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(s1 + (int64_t)y * nx + x));
+#pragma unroll
+          for (int q = 0; q < kBlendVec; q++) t[q] = blend((a4 >> (8 * q)) & 0xFFu, (b4 >> (8 * q)) & 0xFFu);
+        }
+        if (y < yw)
+          surf2DLayeredwrite(make_ushort4((unsigned short)t[0], (unsigned short)t[1], (unsigned short)t[2],
+                                          (unsigned short)t[3]),
+                             surf, x * (int)sizeof(unsigned short), y, layer);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kBlendVec; q++)
+          if (x + q < nx) {
+            t[q] = texel(x + q, y);
+            if (y < yw) surf2DLayeredwrite((unsigned short)t[q], surf, (x + q) * (int)sizeof(unsigned short), y, layer);
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < kBlendVec; q++) cm[q] = max(cm[q], t[q]);
     }
   }
-  colmax[threadIdx.x] = (uint16_t)cm;
+#pragma unroll
+  for (int q = 0; q < kBlendVec; q++) colmax[threadIdx.x * kBlendVec + q] = (uint16_t)cm[q];
   if (threadIdx.x == 0) {  // the dilation column of the CTA's last block
     const int xe = blockIdx.x * kBlendCols + kBlendCols;
     uint32_t ce = 0;
@@ -733,7 +757,7 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
       const int skip = (sk_env && sk_env[0] == '0') ? 0 : 1;
       const int nbx = (int)((nx + kSkip - 1) / kSkip), nby = (int)((ny + kSkip - 1) / kSkip);
       dim3 bg((unsigned)((nx + kBlendCols - 1) / kBlendCols), (unsigned)nby, (unsigned)(row1 - row0));
-      blend_rows_kernel<<<bg, kBlendCols, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx,
+      blend_rows_kernel<<<bg, kBlendThreads, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx,
                                                    (int)row0, rp.surf, rp.bmax, nbx, nby);
       CTP_CUDA_CHECK_LAUNCH("blend_rows_kernel");
       if (v0.mode == CTP_MODE_MIP)
