@@ -446,6 +446,8 @@ def bench_mip(args, device, rank, world, dist):
             "image": "1024^2 RGBA8", "volume": "1024^3 u8 (config-4 generator)", "views_per_batch": 36,
             "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
+            "bound": "texture pipe: one tld4 gather per sample; ncu l1tex data-pipe TEX wavefronts 76% of peak, "
+                     "L1 hit 92% (profiles/r01_render_c4_mip_ncu.txt)",
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + (
                 "" if world == 1 else f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's "
                                       "images over NVLink by the render kernels")}
