@@ -603,7 +603,10 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
 template <typename T, int L, int THREADS, int NST, int MAXU, bool WANT0, bool POW2>
 static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
   constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
-  static_assert(sm <= 227 * 1024 - 4096, "shared memory budget");
+  if constexpr (sm > 227 * 1024 - 4096) {  // a variant that does not fit this table layout
+    set_error("preview: launch shape needs %zu bytes of shared memory", sm);
+    return CTP_E_UNSUPPORTED;
+  } else {
   auto kern = preview_kernel<T, L, THREADS, NST, MAXU, WANT0, POW2>;
   CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   if (a.top != nullptr) {
@@ -624,6 +627,7 @@ static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStrea
   kern<<<grid, THREADS, sm, st>>>(map, a);
   CTP_CUDA_CHECK_LAUNCH("preview_kernel");
   return CTP_OK;
+  }
 }
 
 template <typename T, int L, int THREADS, int NST, int MAXU>
@@ -674,6 +678,7 @@ static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
     case 1: return launch_v<T, L, 512, 2, 1024>(a, vol, st);
     case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
     case 3: return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
+    case 4: return launch_v<T, L, 512, 2, 512>(a, vol, st);
     default:
       if constexpr (sizeof(T) == 1) return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
       else return launch_v<T, L, 512, 2, 1024>(a, vol, st);
