@@ -96,3 +96,23 @@ def test_validation_errors_without_gpu(lib):
 def test_launch_counter_starts_at_zero(lib):
     lib.ctp_launch_count(1)
     assert lib.ctp_launch_count(0) == 0
+
+
+def test_validation_errors_without_gpu_newer_entry_points(lib):
+    # slab rendering: the slab must lie inside the volume
+    view = _lib.View()
+    rc = lib.ctp_render_slab_u8(C.c_void_p(16), 90, 20, 100, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, None)
+    assert rc == _lib.CTP_E_INVALID and "slab" in _err(lib)
+    rc = lib.ctp_render_slab_u8(None, 0, 8, 8, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, None)
+    assert rc == _lib.CTP_E_INVALID
+    # PNG filtering and IPC argument checks
+    rc = lib.ctp_png_filter_u8(None, 1, 4, 4, C.c_void_p(16), None)
+    assert rc == _lib.CTP_E_INVALID
+    rc = lib.ctp_png_filter_u8(C.c_void_p(16), 0, 4, 4, C.c_void_p(16), None)
+    assert rc == _lib.CTP_E_INVALID and "bad shape" in _err(lib)
+    rc = lib.ctp_ipc_import(None, 0, C.byref(C.c_void_p()))
+    assert rc == _lib.CTP_E_INVALID
+    rc = lib.ctp_ipc_close(None, 0)
+    assert rc == _lib.CTP_E_INVALID
+    rc = lib.ctp_ipc_export(None, C.create_string_buffer(64), C.byref(C.c_int64()))
+    assert rc == _lib.CTP_E_INVALID
