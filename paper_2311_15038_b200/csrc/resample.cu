@@ -44,38 +44,54 @@ __global__ void downscale_u8_kernel(const uint8_t* __restrict__ in, int64_t nz, 
   }
 }
 
-// one thread per 4 atlas bytes (or per byte when s % 4 != 0)
-__global__ void encode_atlas_kernel(const uint8_t* __restrict__ cube, int64_t nz, int64_t ny, int64_t nx, int s,
-                                    int grid, int atlas_dim, int map_count, uint8_t* __restrict__ atlases) {
-  const int64_t map_bytes = (int64_t)atlas_dim * atlas_dim;
-  const int64_t total = map_bytes * map_count;
-  const int64_t per = (int64_t)grid * grid;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = o / map_bytes;
-    const int64_t rem = o - m * map_bytes;
-    const int64_t R = rem / atlas_dim, C = rem - (rem / atlas_dim) * atlas_dim;
-    const int64_t cy = R / s, y = R - cy * s;
-    const int64_t cx = C / s, x = C - cx * s;
-    const int64_t k = m * per + cy * grid + cx;
-    uint8_t v = 0;
-    if (k < nz && y < ny && x < nx) v = __ldg(cube + (k * ny + y) * nx + x);
-    atlases[o] = v;
+// One CTA per atlas row (map m, row R of the atlas): every 16-byte chunk of the
+// row is one slice row segment (slice k = m*grid^2 + (R / s)*grid + C / s, row
+// R % s, columns C % s ..) copied with one 16-byte load and store -- or zero
+// where the level is smaller than the cell (_pad_to_cube, pipeline.py:226-237).
+// Byte path when s or the slice rows are not 16-byte granular.
+__global__ void __launch_bounds__(256) encode_atlas_kernel(const uint8_t* __restrict__ cube, int64_t nz, int64_t ny,
+                                                           int64_t nx, int s, int grid, int atlas_dim,
+                                                           uint8_t* __restrict__ atlases) {
+  const int64_t row = blockIdx.x;  // m * atlas_dim + R
+  const int64_t m = row / atlas_dim;
+  const int R = (int)(row - m * atlas_dim);
+  const int cy = R / s, y = R - cy * s;
+  const int64_t k0 = m * (int64_t)grid * grid + (int64_t)cy * grid;  // slice of cell (cy, 0)
+  uint8_t* dst = atlases + row * atlas_dim;
+  const bool vec = (s % 16 == 0) && (nx % 16 == 0) && (atlas_dim % 16 == 0);
+  if (vec) {
+    for (int C = threadIdx.x * 16; C < atlas_dim; C += blockDim.x * 16) {
+      const int cx = C / s, x = C - cx * s;
+      const int64_t k = k0 + cx;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (k < nz && y < ny && x < nx) v = __ldg(reinterpret_cast<const uint4*>(cube + (k * ny + y) * nx + x));
+      *reinterpret_cast<uint4*>(dst + C) = v;
+    }
+  } else {
+    for (int C = threadIdx.x; C < atlas_dim; C += blockDim.x) {
+      const int cx = C / s, x = C - cx * s;
+      const int64_t k = k0 + cx;
+      dst[C] = (k < nz && y < ny && x < nx) ? __ldg(cube + (k * ny + y) * nx + x) : (uint8_t)0;
+    }
   }
 }
 
-__global__ void decode_atlas_kernel(const uint8_t* __restrict__ atlases, int s, int grid, int atlas_dim,
-                                    uint8_t* __restrict__ cube) {
-  const int64_t total = (int64_t)s * s * s;
+// One CTA per cube row (slice k, row y): s bytes gathered from the atlas cell row.
+__global__ void __launch_bounds__(256) decode_atlas_kernel(const uint8_t* __restrict__ atlases, int s, int grid,
+                                                           int atlas_dim, uint8_t* __restrict__ cube) {
+  const int64_t r = blockIdx.x;  // k * s + y
+  const int64_t k = r / s;
+  const int y = (int)(r - k * s);
   const int64_t per = (int64_t)grid * grid;
-  const int64_t map_bytes = (int64_t)atlas_dim * atlas_dim;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t x = o % s;
-    const int64_t r = o / s;
-    const int64_t y = r % s;
-    const int64_t k = r / s;
-    const int64_t m = k / per, w = k - (k / per) * per;
-    const int64_t cy = w / grid, cx = w - (w / grid) * grid;
-    cube[o] = __ldg(atlases + m * map_bytes + (cy * s + y) * atlas_dim + cx * s + x);
+  const int64_t m = k / per, w = k - m * per;
+  const int cy = (int)(w / grid), cx = (int)(w - (w / grid) * grid);
+  const uint8_t* src = atlases + m * (int64_t)atlas_dim * atlas_dim + (int64_t)(cy * s + y) * atlas_dim + cx * s;
+  uint8_t* dst = cube + r * s;
+  if (s % 16 == 0 && atlas_dim % 16 == 0) {
+    for (int x = threadIdx.x * 16; x < s; x += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(dst + x) = __ldg(reinterpret_cast<const uint4*>(src + x));
+  } else {
+    for (int x = threadIdx.x; x < s; x += blockDim.x) dst[x] = __ldg(src + x);
   }
 }
 
@@ -136,9 +152,9 @@ int ctp_encode_atlas_u8(const uint8_t* cube, int64_t nz, int64_t ny, int64_t nx,
   ctp_level_out lo{atlases, CTP_LAYOUT_ATLAS, s, grid, atlas_dim, map_count, 0};
   int rc = check_level_desc(lo, nx, ny, nz, 0);
   if (rc != CTP_OK) return rc;
-  const int64_t total = (int64_t)atlas_dim * atlas_dim * map_count;
-  encode_atlas_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(cube, nz, ny, nx, s, grid, atlas_dim,
-                                                                         map_count, atlases);
+  const int64_t rows = (int64_t)atlas_dim * map_count;
+  CTP_REQUIRE(rows < (1LL << 31), CTP_E_INVALID, "ctp_encode_atlas_u8: too many atlas rows");
+  encode_atlas_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(cube, nz, ny, nx, s, grid, atlas_dim, atlases);
   CTP_CUDA_CHECK_LAUNCH("encode_atlas_kernel");
   return CTP_OK;
 }
@@ -162,8 +178,8 @@ int ctp_decode_atlas_u8(const uint8_t* atlases, int32_t s, int32_t grid, int32_t
   ctp_level_out lo{const_cast<uint8_t*>(atlases), CTP_LAYOUT_ATLAS, s, grid, atlas_dim, map_count, 0};
   int rc = check_level_desc(lo, s, s, s, 0);
   if (rc != CTP_OK) return rc;
-  const int64_t total = (int64_t)s * s * s;
-  decode_atlas_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(atlases, s, grid, atlas_dim, cube);
+  const int64_t rows = (int64_t)s * s;
+  decode_atlas_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(atlases, s, grid, atlas_dim, cube);
   CTP_CUDA_CHECK_LAUNCH("decode_atlas_kernel");
   return CTP_OK;
 }
