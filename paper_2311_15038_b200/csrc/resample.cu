@@ -12,35 +12,106 @@
 
 namespace ctp {
 
-// start[j] = ceil((2 j n - t) / (2 t)), start[0] = 0, start[t] = n (volume.py:265-274)
-__device__ __forceinline__ int64_t cell_start(int64_t j, int64_t n, int64_t t) {
-  if (j <= 0) return 0;
+// start[j] = ceil((2 j n - t) / (2 t)), start[0] = 0, start[t] = n (volume.py:265-274);
+// 32-bit arithmetic (the host keeps n, t < 2^15 so that 2 j n < 2^31)
+__device__ __forceinline__ uint32_t cell_start(uint32_t j, uint32_t n, uint32_t t) {
+  if (j == 0) return 0;
   if (j >= t) return n;
-  const int64_t num = 2 * j * n - t;  // > 0 for j >= 1 since t <= n
-  return (num + 2 * t - 1) / (2 * t);
+  return (2u * j * n - t + 2u * t - 1u) / (2u * t);
 }
 
-__global__ void downscale_u8_kernel(const uint8_t* __restrict__ in, int64_t nz, int64_t ny, int64_t nx,
-                                    int64_t tz, int64_t ty, int64_t tx, uint8_t* __restrict__ out) {
-  const int64_t total = tz * ty * tx;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t jx = o % tx;
-    const int64_t r = o / tx;
-    const int64_t jy = r % ty;
-    const int64_t jz = r / ty;
-    const int64_t xa = cell_start(jx, nx, tx), xb = cell_start(jx + 1, nx, tx);
-    const int64_t ya = cell_start(jy, ny, ty), yb = cell_start(jy + 1, ny, ty);
-    const int64_t za = cell_start(jz, nz, tz), zb = cell_start(jz + 1, nz, tz);
+// One CTA per output row (jz, jy): the row's z and y cell bounds once, each
+// thread sums the cells of its outputs along x (contiguous source segments).
+__global__ void __launch_bounds__(256) downscale_u8_kernel(const uint8_t* __restrict__ in, int nz, int ny, int nx,
+                                                           int tz, int ty, int tx, uint8_t* __restrict__ out) {
+  const int64_t row = blockIdx.x;  // jz * ty + jy
+  const uint32_t jz = (uint32_t)(row / ty), jy = (uint32_t)(row - (int64_t)jz * ty);
+  const uint32_t ya = cell_start(jy, ny, ty), yb = cell_start(jy + 1, ny, ty);
+  const uint32_t za = cell_start(jz, nz, tz), zb = cell_start(jz + 1, nz, tz);
+  const uint32_t cyz = (yb - ya) * (zb - za);
+  for (uint32_t jx = threadIdx.x; jx < (uint32_t)tx; jx += blockDim.x) {
+    const uint32_t xa = cell_start(jx, nx, tx), xb = cell_start(jx + 1, nx, tx);
     uint64_t acc = 0;
-    for (int64_t z = za; z < zb; z++)
-      for (int64_t y = ya; y < yb; y++) {
-        const uint8_t* row = in + (z * ny + y) * nx;
+    for (uint32_t z = za; z < zb; z++)
+      for (uint32_t y = ya; y < yb; y++) {
+        const uint8_t* r = in + ((int64_t)z * ny + y) * nx;
         uint32_t rs = 0;
-        for (int64_t x = xa; x < xb; x++) rs += __ldg(row + x);
+        for (uint32_t x = xa; x < xb; x++) rs += __ldg(r + x);
         acc += rs;
       }
-    const uint64_t cnt = (uint64_t)(xb - xa) * (uint64_t)(yb - ya) * (uint64_t)(zb - za);
-    out[o] = (uint8_t)((2 * acc + cnt) / (2 * cnt));  // volume.py:306-308 round half up
+    const uint64_t cnt = (uint64_t)(xb - xa) * cyz;
+    out[row * tx + jx] = (uint8_t)((2 * acc + cnt) / (2 * cnt));  // volume.py:306-308 round half up
+  }
+}
+
+// Vector path of the same (16-byte rows, cells of <= 257 source rows, nx <= 16384):
+// each thread owns 16 source columns, sums them over the output row's (z, y)
+// cell rows in packed 16-bit lanes (even / odd bytes of each word), spills the
+// column sums to shared memory, and the outputs of the row then sum their
+// x-cells from there.  Every source byte is read once, with 16-byte loads.
+__global__ void __launch_bounds__(256) downscale_u8_vec_kernel(const uint8_t* __restrict__ in, int nz, int ny, int nx,
+                                                               int tz, int ty, int tx, int tpr,
+                                                               uint8_t* __restrict__ out) {
+  extern __shared__ uint32_t colsum_all[];  // (256 / tpr) rows x (nx + 16), then the tx + 1 x-cell starts
+  // tpr threads per output row, 256 / tpr output rows at a time per CTA (grid-stride)
+  const int rpc = blockDim.x / tpr;
+  uint32_t* xs = colsum_all + (int64_t)rpc * (nx + 16);  // the x partition is the same for every row
+  for (int j = threadIdx.x; j <= tx; j += blockDim.x) xs[j] = cell_start(j, nx, tx);
+  __syncthreads();
+  const int g = threadIdx.x / tpr, t = threadIdx.x - g * tpr;
+  const int nc = nx / 16;  // 16-byte column chunks
+  // column x lives at (x % 16) * (nc + 1) + x / 16: the 16 stores of a thread and
+  // the x-cell reads of neighbouring outputs both spread over the banks
+  uint32_t* colsum = colsum_all + (int64_t)g * (nx + 16);
+  const int64_t rows = (int64_t)ty * tz;
+  for (int64_t base = (int64_t)blockIdx.x * rpc; base < rows; base += (int64_t)gridDim.x * rpc) {
+    const int64_t row = base + g;  // jz * ty + jy
+    const bool live = row < rows;
+    uint32_t ya = 0, yb = 0, za = 0, zb = 0;
+    if (live) {
+      const uint32_t jz = (uint32_t)(row / ty), jy = (uint32_t)(row - (int64_t)jz * ty);
+      ya = cell_start(jy, ny, ty);
+      yb = cell_start(jy + 1, ny, ty);
+      za = cell_start(jz, nz, tz);
+      zb = cell_start(jz + 1, nz, tz);
+      for (int c = t; c < nc; c += tpr) {
+        uint32_t ev[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
+        for (uint32_t z = za; z < zb; z++)
+          for (uint32_t y = ya; y < yb; y++) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + ((int64_t)z * ny + y) * nx + 16 * c));
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+              ev[i] += w[i] & 0x00FF00FFu;
+              od[i] += (w[i] >> 8) & 0x00FF00FFu;
+            }
+          }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          colsum[(4 * i + 0) * (nc + 1) + c] = ev[i] & 0xFFFFu;
+          colsum[(4 * i + 1) * (nc + 1) + c] = od[i] & 0xFFFFu;
+          colsum[(4 * i + 2) * (nc + 1) + c] = ev[i] >> 16;
+          colsum[(4 * i + 3) * (nc + 1) + c] = od[i] >> 16;
+        }
+      }
+    }
+    __syncthreads();
+    if (live) {
+      const uint32_t cyz = (yb - ya) * (zb - za);
+      for (uint32_t jx = t; jx < (uint32_t)tx; jx += tpr) {
+        const uint32_t xa = xs[jx], xb = xs[jx + 1];
+        uint32_t acc = 0;
+        for (uint32_t x = xa; x < xb; x++) acc += colsum[(x & 15) * (nc + 1) + (x >> 4)];
+        // floor((2 acc + cnt) / (2 cnt)) (volume.py:306-308, round half up), <= 255: a float
+        // estimate corrected to the exact integer quotient (cnt <= 257 * 16384: 32-bit safe)
+        const uint32_t cnt = (xb - xa) * cyz, num = 2u * acc + cnt, den = 2u * cnt;
+        uint32_t q = (uint32_t)__fmul_rz((float)num, __frcp_rn((float)den));
+        if ((q + 1) * den <= num) q++;
+        if (q * den > num) q--;
+        out[row * tx + jx] = (uint8_t)q;
+      }
+    }
+    __syncthreads();  // colsum is rewritten by the next rows
   }
 }
 
@@ -140,8 +211,28 @@ int ctp_downscale_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, int6
     CTP_CUDA_CALL(cudaMemcpyAsync(out, in, (size_t)(nx * ny * nz), cudaMemcpyDeviceToDevice, st));
     return CTP_OK;
   }
-  const int64_t total = tx * ty * tz;
-  downscale_u8_kernel<<<grid1d(total, 256), 256, 0, st>>>(in, nz, ny, nx, tz, ty, tx, out);
+  CTP_REQUIRE(nx < 32768 && ny < 32768 && nz < 32768, CTP_E_UNSUPPORTED,
+              "ctp_downscale_u8: axes of 32768 or more voxels are not supported (32-bit cell bounds)");
+  // the vector path needs 16-byte rows, <= 257 source rows per cell (packed 16-bit
+  // column sums) and the column sums of one row in shared memory
+  const int64_t cell_rows = ((ny + ty - 1) / ty + 1) * ((nz + tz - 1) / tz + 1);
+  if (nx % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 && nx <= 16384 && cell_rows <= 257) {
+    int tpr = 32;  // threads per output row: one 16-byte column chunk each, <= 256
+    while (tpr < 256 && tpr * 16 < nx) tpr *= 2;
+    const int rpc = 256 / tpr;
+    const size_t sm = ((size_t)rpc * (nx + 16) + (size_t)tx + 1) * sizeof(uint32_t);
+    if (sm > 48 * 1024)
+      CTP_CUDA_CALL(cudaFuncSetAttribute(downscale_u8_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int64_t rows = ty * tz;
+    int64_t blocks = (rows + rpc - 1) / rpc;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    downscale_u8_vec_kernel<<<(unsigned)blocks, 256, sm, st>>>(in, (int)nz, (int)ny, (int)nx, (int)tz, (int)ty,
+                                                               (int)tx, tpr, out);
+    CTP_CUDA_CHECK_LAUNCH("downscale_u8_vec_kernel");
+    return CTP_OK;
+  }
+  downscale_u8_kernel<<<(unsigned)(ty * tz), 256, 0, st>>>(in, (int)nz, (int)ny, (int)nx, (int)tz, (int)ty, (int)tx,
+                                                          out);
   CTP_CUDA_CHECK_LAUNCH("downscale_u8_kernel");
   return CTP_OK;
 }

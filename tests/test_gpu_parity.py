@@ -121,6 +121,21 @@ def test_downscale_random_ratios(P):
         assert np.array_equal(P.downscale_volume(P.Volume(v), target).voxels, O.downscale(v, target)), (shape, target)
 
 
+def test_downscale_vector_path_general_ratios(P, cuda):
+    """16-byte rows take the column-sum kernel (packed 16-bit lanes); incl. cells of
+    up to 16x16 source rows (255 * 256 per lane) and extreme x ratios."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(9)
+    # targets are (tx, ty, tz), shapes (nz, ny, nx) as everywhere in the reference
+    for shape, target in [((40, 36, 64), (37, 23, 17)), ((64, 48, 160), (128, 7, 5)), ((256, 256, 32), (2, 16, 16)),
+                          ((16, 16, 4096), (999, 16, 1)), ((33, 70, 4096), (999, 3, 1)), ((17, 255, 48), (48, 16, 17)),
+                          ((8, 8, 16384), (5000, 8, 8))]:
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        v[:, :, :16] = 255  # saturated columns: the packed lanes at their maximum
+        got = dev.downscale(torch.from_numpy(v).to(cuda), target).cpu().numpy()
+        assert np.array_equal(got, O.downscale(v, target)), (shape, target)
+
+
 def test_errors_match_reference(P):
     v = P.Volume(np.zeros((4, 4, 4), np.uint8))
     with pytest.raises(P.InvalidTarget):
