@@ -10,12 +10,16 @@ ONE cooperative launch (artifact-LUT phase, grid barrier, fused pass).
            pinned host atlases + histogram out, PCIe copies inside the timed region)
   mip    = config-4 MIP frames/s (36 azimuths, 1024^2 RGBA8, 0.5-voxel steps, 1024^3)
 
-Multi-GPU (torchrun, --gpus N): the SAME 1024^3 volume is split into N z-slabs
-(strong scaling; slab heights are whole 2^3 cells and whole atlas cell rows,
-so no halo): the artifact LUT is broadcast from the rank holding the top
-slices, histograms are all-reduced (NCCL), and every rank's fused pass stores
-its atlas cell rows straight into rank 0's atlases through a CUDA IPC mapping
-over NVLink -- the gather is part of the pass (paper_2311_15038_b200/dist.py).
+Multi-GPU (torchrun, --gpus N): the headline is weak -- every GPU reduces its
+own c2 scan (independent objects, no data-path collective), value = all ranks'
+voxels / the slowest rank's time.  Side measurement "c2_zslab" (strong): ONE
+1024^3 volume split into N z-slabs (heights whole 2^3 cells and atlas cell
+rows, no halo): the artifact LUT broadcast from the rank holding the top
+slices, histograms all-reduced (NCCL), and every rank's fused pass storing its
+atlas cell rows straight into rank 0's atlases through a CUDA IPC mapping over
+NVLink -- the gather is part of the pass (paper_2311_15038_b200/dist.py).
+MIP likewise: replicas (headline) and "sort_last" (one volume, z-slab bands
+stored into rank 0's images by the render kernels).
 
 ``--impl reference``: the reference's CPU algorithm (the numpy oracle port of
 ctprev) on the box's host cores, process pool over z-slabs, bounded sample.
@@ -238,10 +242,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (the modulo only matters for a functional run of N ranks on fewer GPUs with
+    # CTP_BENCH_BACKEND=gloo -- never a timing; on a node every rank has its GPU)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("CTP_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": device} if backend == "nccl" else {}))
 
     from paper_2311_15038_b200 import _lib, synth
     from paper_2311_15038_b200.device import AtlasSpec
@@ -256,10 +264,11 @@ def main():
     plan = plan_preview(spec.shape, schemes)
     assert not plan.general and plan.nlev == 3
     level_of = dict(plan.scheme_level)
-    # N > 1: the atlas gather is fused into the pass (ranks > 0 store into rank 0's atlases over NVLink)
-    sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), rank, world,
-                        device, peer_atlases=True)
-    slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)  # this rank's z-slab
+    # headline: every GPU reduces its own c2 scan (N > 1: independent scans, weak scaling, no
+    # data-path collective); the z-slab sharding of ONE volume across the N GPUs is the
+    # side measurement "c2_zslab" below
+    sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), 0, 1, device)
+    slab = synth.generate(synth.config("c2", seed=rank), device=device)  # this GPU's scan
     stream = torch.cuda.current_stream()
     k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -300,7 +309,7 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = nx * ny * nz * args.steps / (ms * 1e-3) / 1e9   # the whole volume per step, all ranks together
+    value = world * nx * ny * nz * args.steps / (ms * 1e-3) / 1e9   # every rank's volume per step, all ranks
     assert int(res["hist"].sum().item()) == nx * ny * nz     # the all-reduced histogram covers every voxel
 
     # roofline of the dominant kernel (the fused pass), this rank's slab
@@ -321,11 +330,9 @@ def main():
     # ---- e2e through the host-buffer session (pinned host slab in, pinned atlases out)
     e2e = None
     if not args.no_e2e:
-        sess = PreviewSession((sh.z1 - sh.z0, ny, nx) if world == 1 else spec.shape, torch.uint8, schemes,
-                              chunk_slices=64, device=device)
+        sess = PreviewSession(spec.shape, torch.uint8, schemes, chunk_slices=64, device=device)
         host = torch.empty(sess.shape, dtype=torch.uint8, pin_memory=True)
-        if world == 1:
-            host.copy_(slab)
+        host.copy_(slab)
         for _ in range(2):
             sess.run(host)
         e_steps = 10
@@ -345,9 +352,44 @@ def main():
         e2e = {"value": vox_e2e * e_steps / e_s / 1e9, "unit": "GVoxel/s",
                "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes, "steps": e_steps,
                "path": "PreviewSession.run(pinned host volume): z-chunk streamed H2D / fused pass / atlas D2H on "
-                       "3 CUDA streams" + ("" if world == 1 else "; one full volume per rank")}
+                       "3 CUDA streams" + ("" if world == 1 else "; one scan per rank")}
         del sess, host
         torch.cuda.empty_cache()
+
+    # ---- N > 1: ONE c2 volume z-slab sharded across the ranks (strong scaling): LUT broadcast
+    # from the top-slab owner, fused pass per slab storing its atlas rows into rank 0's atlases
+    # over NVLink (CUDA IPC), histogram all-reduce -- SURVEY s8(e)
+    zslab = None
+    if world > 1:
+        del slab
+        torch.cuda.empty_cache()
+        shz = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), rank, world,
+                             device, peer_atlases=True)
+        zs = synth.generate(spec, z_range=(shz.z0, shz.z1), device=device)
+        for _ in range(max(3, args.warmup // 4)):
+            shz.step(zs)
+        zsteps = max(10, min(args.steps, 100))
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(zsteps):
+            rz = shz.step(zs)
+        a1.record()
+        torch.cuda.synchronize()
+        zt = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=device)
+        dist.all_reduce(zt, op=dist.ReduceOp.MAX)
+        zms = float(zt.item()) / zsteps
+        assert int(rz["hist"].sum().item()) == nx * ny * nz
+        zslab = {"workload": "c2 (one 1024^3 volume) z-slab sharded across the ranks", "scaling": "strong",
+                 "ms_per_step": zms, "gvoxel_per_s": nx * ny * nz / zms / 1e6, "slab": [shz.z0, shz.z1],
+                 "collectives": "LUT broadcast (NCCL), histogram all-reduce (NCCL), atlas rows stored into rank 0's "
+                                "atlases by the fused kernels over NVLink (CUDA IPC)"}
+        shz.close()
+        del zs, shz
+        torch.cuda.empty_cache()
+        slab = synth.generate(synth.config("c2", seed=rank), device=device)
 
     # ---- CPU baseline (rank 0, N=1 only): the oracle port on all host cores, bounded sample
     cpu = None
@@ -372,6 +414,8 @@ def main():
         del slab
         torch.cuda.empty_cache()
         mip = bench_mip(args, device, rank, world, dist)
+        if world > 1:
+            mip["sort_last"] = bench_mip(args, device, rank, world, dist, sort_last=True)
     others = None
     if not args.no_configs and world == 1:
         torch.cuda.empty_cache()
@@ -380,11 +424,12 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GVoxel/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded config-2 generator, on device)",
             "config": {"workload": "c2: 1024^3 u8, hist + artifact-bin filter + 512/256/128 levels + slicemap "
                                    "atlases (8x4096^2, 4x2048^2, 2x1024^2)",
-                       "voxels_per_step": nx * ny * nz, "parallelism": f"z-slab x{world}",
+                       "voxels_per_step": world * nx * ny * nz,
+                       "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (one c2 scan per GPU)",
                        "l2": "input 1 GiB per step > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
@@ -396,6 +441,7 @@ def main():
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "mip": mip,
+            "c2_zslab": zslab,
             "other_configs": others,
         }
         print(json.dumps(line))
@@ -404,21 +450,25 @@ def main():
     return 0
 
 
-def bench_mip(args, device, rank, world, dist):
-    """Config 4: 36 MIP azimuths, 1024^2 RGBA8.  At N > 1 the volume is z-slab
-    sharded and rendered sort-last (each rank its row band from its slab + halo,
-    bands gathered to rank 0 inside the timed region); at N = 1 the whole volume."""
+def bench_mip(args, device, rank, world, dist, sort_last: bool = False):
+    """Config 4: 36 MIP azimuths, 1024^2 RGBA8.  Default: every GPU renders the
+    turntable of its own volume (N > 1: replicas, weak).  ``sort_last``: ONE
+    volume z-slab sharded across the ranks, each rank rendering its row band from
+    its slab + halo and storing it into rank 0's images over NVLink (strong)."""
     import math
     import torch
     from paper_2311_15038_b200 import synth
     from paper_2311_15038_b200.dist import DeviceRenderCompute, ShardedRender
     from paper_2311_15038_b200.types import ViewParams
-    spec = synth.config("c4")
+    spec = synth.config("c4", seed=0 if sort_last else rank)
     n = spec.shape[0]
     dim = 1024
     steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * n)  # 0.5-voxel step over the 2R window: 3548 for 1024^3
     views = [ViewParams(azimuth_deg=10.0 * k, image_dim=dim, steps=steps, mode="mip") for k in range(36)]
-    sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
+    if sort_last:
+        sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
+    else:
+        sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), 0, 1, device)
     local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
     sr.render(local, views, channels=4, fp32=True)   # warmup (row planes allocated once)
     torch.cuda.synchronize()
@@ -436,8 +486,9 @@ def bench_mip(args, device, rank, world, dist):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    frames = 36 * args.mip_batches
+    frames = 36 * args.mip_batches * (1 if sort_last else world)
     del local
+    sr.close()
     from paper_2311_15038_b200 import device as dev
     dev.render_release()
     torch.cuda.empty_cache()
@@ -448,9 +499,11 @@ def bench_mip(args, device, rank, world, dist):
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
             "bound": "texture pipe: one tld4 gather per sample; ncu l1tex data-pipe TEX wavefronts 76% of peak, "
                      "L1 hit 92% (profiles/r01_render_c4_mip_ncu.txt)",
+            "scaling": "strong" if sort_last else "weak",
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + (
-                "" if world == 1 else f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's "
-                                      "images over NVLink by the render kernels")}
+                f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's images over "
+                "NVLink by the render kernels" if sort_last else ("" if world == 1 else
+                                                                  f"; replicas x{world} (one volume per GPU)"))}
 
 
 def _time_steps(fn, reps: int, warmup: int = 2):
