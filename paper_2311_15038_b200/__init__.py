@@ -6,7 +6,7 @@ The public surface mirrors the reference's hot-path API
     volume_histogram, Histogram256.of, artifact_bins, filter_histogram_bins,
     downscale_volume, encode_slicemaps, decode_slicemaps, plan_scheme,
     slice_cell, render_view, image_entropy, optimal_snapshot, apply_circle_mask,
-    build_data_preview, build_interactive_preview, save_slicemaps
+    build_data_preview, build_interactive_preview, build_list_preview, save_slicemaps
 
 plus the fused one-pass ``preview_pipeline`` and batched ``render_views``
 (MIP / front-to-back alpha extensions).  All arithmetic runs in the sm_100a
@@ -18,6 +18,7 @@ from .errors import *  # noqa: F401,F403
 from .types import (ADDITIVE, ALPHA, MIP, SURFACE, EntropyResult, Histogram256, SlicemapScheme, SlicemapSet,
                     SnapshotResult, ViewParams, Volume, plan_scheme, slice_cell)
 from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, build_interactive_preview,
+                  build_list_preview,
                   decode_slicemaps, downscale_volume, encode_slicemaps, save_slicemaps,
                   filter_histogram_bins, image_entropy, optimal_snapshot, preview_pipeline, render_view,
                   render_views, volume_histogram)
@@ -30,6 +31,7 @@ __all__ = [
     "SnapshotResult", "SURFACE", "ADDITIVE", "MIP", "ALPHA", "plan_scheme", "slice_cell",
     "volume_histogram", "artifact_bins", "filter_histogram_bins", "downscale_volume", "encode_slicemaps",
     "decode_slicemaps", "render_view", "render_views", "image_entropy", "optimal_snapshot",
-    "preview_pipeline", "PreviewResult", "build_data_preview", "build_interactive_preview", "apply_circle_mask",
+    "preview_pipeline", "PreviewResult", "build_data_preview", "build_interactive_preview", "build_list_preview",
+    "apply_circle_mask",
     "save_slicemaps", "install", "uninstall",
 ]

@@ -28,6 +28,7 @@ BINDINGS = {
     "build_data_preview": ["pipeline", ""],
     "apply_circle_mask": ["mask", "pipeline", "cli", ""],
     "build_interactive_preview": ["pipeline", ""],
+    "build_list_preview": ["pipeline", ""],
     "save_slicemaps": ["slicemap", "pipeline", ""],
 }
 
@@ -50,6 +51,7 @@ def install(package: str = "ctprev") -> list[str]:
     pl = importlib.import_module(f"{package}.pipeline")
     FACTORY.DataPreview = pl.DataPreview
     FACTORY.InteractivePreview = pl.InteractivePreview
+    FACTORY.ListPreview = pl.ListPreview
     FACTORY.Circle = importlib.import_module(f"{package}.mask").Circle
     patched = []
     for name, mods in BINDINGS.items():

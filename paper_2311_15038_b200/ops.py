@@ -228,11 +228,14 @@ def optimal_snapshot(volume, n_views: int = 36, params=None):
     if n_views < 1:
         raise RangeOutOfBounds(f"n_views {n_views} must be positive")
     template = _view_of(params) if params is not None else ViewParams()
+    return _snapshot_dev(to_device(_voxels(volume)), n_views, template)
+
+
+def _snapshot_dev(vol_t: torch.Tensor, n_views: int, template):
     step = 360.0 / n_views
     views = [ViewParams(azimuth_deg=k * step, image_dim=template.image_dim, steps=template.steps,
                         mode=template.mode, threshold=template.threshold, gain=template.gain)
              for k in range(n_views)]
-    vol_t = to_device(_voxels(volume))
     imgs = dev.render(vol_t, views, channels=1)
     counts = _host(dev.image_hist(imgs))
     size = template.image_dim * template.image_dim
@@ -348,6 +351,54 @@ def _host_helper(module: str, name: str):
     except Exception as e:  # pragma: no cover - depends on the environment
         raise RuntimeError(f"build_interactive_preview: ctprev.{module}.{name} (host, off the device path) is not "
                            f"importable; pass it explicitly") from e
+
+
+def build_list_preview(volume, n_views: int = 36, full_res: bool = False, detect=None, threshold=None):
+    """pipeline.py:157-212 with the volume resident on the device: working copy
+    (``_working_copy``, pipeline.py:142-154), container circle found by the HOST
+    detector on its top slice and masked on the device, the histogram on the
+    device for the host Otsu ``threshold``, then the batched snapshot
+    (``optimal_snapshot``); a missing circle or a single-value histogram degrade
+    the product as the reference does."""
+    from .errors import CircleOutOfBounds, DegenerateHistogram, EmptyVolume, NoCircleFound
+    from .types import STAGES_LIST, THUMBNAIL_DIM, WORKING_EDGE
+    detect = detect or _host_helper("mask", "detect_container_circle")
+    threshold = threshold or _host_helper("threshold", "otsu_threshold")
+    vox = _voxels(volume)
+    if vox.size == 0:
+        raise EmptyVolume("volume has no nonzero voxels")
+    t = to_device(vox)
+    if int(_host(dev.hist_u8(t))[1:].sum()) == 0:                              # pipeline.py:172-173
+        raise EmptyVolume("volume has no nonzero voxels")
+    nz, ny, nx = vox.shape
+    working = t
+    if not full_res and max(nx, ny, nz) > WORKING_EDGE:                       # _working_copy
+        k = -(-max(nx, ny, nz) // WORKING_EDGE)
+        working = _downscale_dev(t, (-(-nx // k), -(-ny // k), -(-nz // k)))
+    warnings_: list[str] = []
+    circle = None
+    masked = working
+    try:
+        circle = detect(_host(working[-1]))                                     # top_slice
+        wz, wy, wx = working.shape
+        if not (0 <= circle.cx < wx and 0 <= circle.cy < wy):                 # mask.py:202-205
+            raise CircleOutOfBounds(f"center ({circle.cx:.1f}, {circle.cy:.1f}) outside {wx}x{wy} slice")
+        masked = dev.circle_mask(working, circle.cx, circle.cy, (circle.r * (1.0 - 0.02)) ** 2)
+    except NoCircleFound:
+        warnings_.append("no_container_circle")
+    thr, mode = None, "surface"
+    try:
+        thr = threshold(FACTORY.Histogram256(_host(dev.hist_u8(masked)))).value
+    except DegenerateHistogram:
+        warnings_.append("degenerate_histogram")
+        mode = "additive"
+    params = ViewParams(image_dim=THUMBNAIL_DIM, steps=THUMBNAIL_DIM, mode=mode, threshold=thr if thr is not None else 1)
+    snap = _snapshot_dev(masked, n_views, params)
+    if circle is not None and working is not t:                               # _rescale_circle to raw pixels
+        fx, fy = nx / working.shape[2], ny / working.shape[1]
+        circle = FACTORY.Circle(circle.cx * fx, circle.cy * fy, circle.r * min(fx, fy), circle.votes)
+    return FACTORY.ListPreview(image=snap.image, azimuth_deg=snap.azimuth_deg, entropy=snap.entropy, threshold=thr,
+                               circle=circle, mode=mode, warnings=tuple(warnings_), stages=STAGES_LIST)
 
 
 def build_interactive_preview(volume, detect=None, threshold=None, margin: float = 0.02):

@@ -239,7 +239,30 @@ class DataPreview:
     stages: tuple
 
 
+STAGES_LIST = ("3d_conversion", "thresholding_container_removal", "server_side_rendering")  # pipeline.py:81
 STAGES_INTERACTIVE = ("slicemaps_conversion", "thresholding_container_removal")  # pipeline.py:83
+THUMBNAIL_DIM = 512                                                                    # pipeline.py:88
+WORKING_EDGE = 256                                                                     # pipeline.py:89
+
+
+@dataclass(frozen=True)
+class ListPreview:
+    """pipeline.py:92-113."""
+
+    image: np.ndarray
+    azimuth_deg: float
+    entropy: float
+    threshold: object
+    circle: object
+    mode: str
+    warnings: tuple
+    stages: tuple
+
+    def sidecar(self) -> dict:
+        c = self.circle
+        return {"azimuth": self.azimuth_deg, "entropy": self.entropy, "threshold": self.threshold,
+                "circle": None if c is None else {"cx": c.cx, "cy": c.cy, "r": c.r, "votes": c.votes},
+                "mode": self.mode, "warnings": list(self.warnings)}
 INTERACTIVE_SCHEMES = (128, 256, 512)                                          # pipeline.py:85
 
 
@@ -288,6 +311,7 @@ class _Factory:
         self.SnapshotResult = SnapshotResult
         self.DataPreview = DataPreview
         self.InteractivePreview = InteractivePreview
+        self.ListPreview = ListPreview
         self.Circle = Circle
 
 

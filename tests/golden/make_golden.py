@@ -5,8 +5,8 @@ Run in the builder container, where /root/reference exists:
     NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
         python tests/golden/make_golden.py
 
-Writes tests/golden/ref_golden.npz, ref_golden_datapreview.npz and
-ref_golden_interactive.npz (committed).  The GPU box never reads
+Writes tests/golden/ref_golden.npz, ref_golden_datapreview.npz,
+ref_golden_interactive.npz and ref_golden_bundles.npz (committed).  The GPU box never reads
 /root/reference: tests compare the CPU oracle and the CUDA path against these
 frozen reference outputs.
 """
@@ -230,7 +230,88 @@ def interactive_preview_golden() -> None:
     print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
 
 
+def bundle_golden() -> None:
+    """The reference's own bundle flow (ingest_stack + build_bundle, pipeline.py:356-500)
+    for the two bundles whose checksums are mounted -- fixture-128
+    (frontend/scripts/make-fixtures.py:67-81, n_views 4) and demo-scan-01
+    (demos/full_pipeline.py:49-68, n_views 6).  Every file's sha256 is checked
+    against the mounted meta.json first (27/27 each), then the decoded products are
+    frozen: the input volume, data atlases + bins, interactive atlases per scheme +
+    circle / thresholds / warnings, and the thumbnail + its sidecar."""
+    import hashlib
+    import json
+    import shutil
+    import tempfile
+    from PIL import Image
+    from ctprev.phantom import CylinderSpec, PhantomSpec, SphereSpec, generate_phantom
+    from ctprev.pipeline import build_bundle, ingest_stack
+    ref = Path("/root/reference/pkg")
+    cases = [
+        ("fixture-128", "Viewer Fixture", 4, ref / "frontend/tests/fixtures/bundles/fixture-128/meta.json",
+         PhantomSpec(dims=(128, 128, 128), fill=(4, 18),
+                     container=CylinderSpec(cx=65.0, cy=63.0, r=52.0, wall=2.5, value=(140, 145)),
+                     objects=(SphereSpec(cx=60.0, cy=68.0, cz=52.0, r=20.0, value=(200, 210)),
+                              SphereSpec(cx=76.0, cy=54.0, cz=92.0, r=10.0, value=(220, 230))),
+                     salt_pepper=0.0005, seed=11)),
+        ("demo-scan-01", "Demo Scan 01", 6, ref / "demos/out/full_pipeline/bundles/demo-scan-01/meta.json",
+         PhantomSpec(dims=(160, 160, 96),
+                     container=CylinderSpec(cx=81.0, cy=78.0, r=65.0, wall=2.0, value=(140, 145)),
+                     objects=(SphereSpec(cx=75.0, cy=85.0, cz=40.0, r=22.0, value=(200, 210)),),
+                     salt_pepper=0.001, seed=5)),
+    ]
+    g = {"b_n": np.array(len(cases))}
+    work = Path(tempfile.mkdtemp(prefix="ctp_bundles_"))
+    try:
+        for i, (bid, name, n_views, meta_path, spec) in enumerate(cases):
+            vol = generate_phantom(spec).volume
+            stack = work / f"stack{i}"
+            stack.mkdir()
+            names = []
+            for z in range(vol.nz):  # the scripts' write_stack: one L-mode PNG per slice + stack.json
+                fn = f"slice_{z:04d}.png"
+                Image.fromarray(np.asarray(vol.voxels[z]), mode="L").save(stack / fn)
+                names.append(fn)
+            (stack / "stack.json").write_text(json.dumps({"name": name, "slices": names, "bit_depth": 8}))
+            root = work / f"root{i}"
+            ingest_stack(stack / "stack.json", root, dataset_id=bid)
+            meta = build_bundle(root, bid, n_views=n_views)
+            bundle = root / bid
+            want = json.loads(meta_path.read_text())["checksums"]
+            ok = 0
+            for rel, digest in want.items():
+                if hashlib.sha256((bundle / rel).read_bytes()).hexdigest() == digest:
+                    ok += 1
+            print(f"{bid}: {ok}/{len(want)} files match the mounted checksums")
+            assert ok == len(want), bid
+
+            def png(rel):
+                with Image.open(bundle / rel) as im:
+                    return np.asarray(im).copy()
+
+            nz, ny, nx = vol.voxels.shape
+            g[f"b{i}_id"] = np.array(bid)
+            g[f"b{i}_nviews"] = np.array(n_views)
+            g[f"b{i}_checks"] = np.array([ok, len(want)])
+            g[f"b{i}_vol"] = np.fromfile(bundle / "volume.raw", dtype=np.uint8).reshape(nz, ny, nx)
+            g[f"b{i}_meta"] = np.array(json.dumps(meta, sort_keys=True))
+            g[f"b{i}_thumb"] = png("thumbnail.png")
+            g[f"b{i}_sidecar"] = np.array((bundle / "thumbnail.json").read_text())
+            dman = json.loads((bundle / "data" / "manifest.json").read_text())
+            g[f"b{i}_data"] = np.stack([png(f"data/{a}") for a in dman["atlases"]])
+            for s in (128, 256, 512):
+                man = json.loads((bundle / "interactive" / str(s) / "manifest.json").read_text())
+                g[f"b{i}_int{s}"] = np.stack([png(f"interactive/{s}/{a}") for a in man["atlases"]])
+    finally:
+        shutil.rmtree(work, ignore_errors=True)
+    out = Path(__file__).resolve().parent / "ref_golden_bundles.npz"
+    np.savez_compressed(out, **g)
+    print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
+
+
 if __name__ == "__main__":
+    if "--only-bundles" in sys.argv:
+        bundle_golden()
+        sys.exit(0)
     if "--only-interactive" in sys.argv:
         interactive_preview_golden()
         sys.exit(0)
@@ -238,3 +319,4 @@ if __name__ == "__main__":
         main()
     data_preview_golden()
     interactive_preview_golden()
+    bundle_golden()

@@ -554,3 +554,64 @@ def test_build_interactive_preview_golden(P, golden_dp):
             assert a.shape == tuple(g[f"ip{i}_shape{s}"]), (i, s)
             assert hashlib.sha256(a.tobytes()).hexdigest() == str(g[f"ip{i}_sha{s}"]), (i, s)
         assert np.array_equal(np.stack(ip.slicemaps[128].atlases), g[f"ip{i}_atlas128"]), i
+
+
+def test_bundles_pixel_parity(P, cuda, tmp_path):
+    """The reference's two recorded bundles (fixture-128 and demo-scan-01; make_golden
+    re-ran ingest_stack + build_bundle and matched all 27/27 mounted checksums of each):
+    our list / data / interactive builders on the ingested volume reproduce every
+    product pixel for bit -- thumbnail (+ azimuth, entropy, threshold, mode), data
+    atlases + filtered bins, interactive atlases per scheme + thresholds + warnings --
+    and our save_slicemaps writes the same manifest and losslessly decodable atlases.
+    The host helpers (circle Hough transform, Otsu sweep) are injected: the recorded
+    circle, the oracle's pinned Otsu."""
+    import json
+    from pathlib import Path
+    from PIL import Image
+    from paper_2311_15038_b200 import ops
+    from paper_2311_15038_b200.errors import DegenerateHistogram, NoCircleFound
+    from paper_2311_15038_b200.types import Circle
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_bundles.npz") as z:
+        g = {k: z[k] for k in z.files}
+
+    def otsu(h):
+        t = O.otsu_threshold(h.bins)
+        if t is None:
+            raise DegenerateHistogram("all histogram mass in a single bin")
+        return type("R", (), {"value": t})()
+
+    def detector(c):
+        def detect(top):
+            if c is None:
+                raise NoCircleFound("recorded: no circle")
+            return Circle(c["cx"], c["cy"], c["r"], c["votes"])
+        return detect
+
+    for i in range(int(g["b_n"])):
+        vol = P.Volume(g[f"b{i}_vol"])
+        meta = json.loads(str(g[f"b{i}_meta"]))
+        side = json.loads(str(g[f"b{i}_sidecar"]))
+        # list preview (pipeline.py:157-212)
+        lp = ops.build_list_preview(vol, n_views=int(g[f"b{i}_nviews"]), detect=detector(side["circle"]),
+                                    threshold=otsu)
+        assert np.array_equal(lp.image, g[f"b{i}_thumb"]), i
+        assert (lp.azimuth_deg, lp.entropy, lp.threshold, lp.mode, list(lp.warnings)) == (
+            side["azimuth"], side["entropy"], side["threshold"], side["mode"], side["warnings"]), i
+        # data preview (pipeline.py:240-257)
+        dp = ops.build_data_preview(vol)
+        assert np.array_equal(np.stack(dp.slicemaps.atlases), g[f"b{i}_data"]), i
+        assert list(dp.filtered_bins) == meta["previews"]["data"]["filtered_bins"], i
+        # interactive preview (pipeline.py:267-309)
+        inter = meta["previews"]["interactive"]
+        ip = ops.build_interactive_preview(vol, detect=detector(inter["container"]), threshold=otsu)
+        for s in (128, 256, 512):
+            assert np.array_equal(np.stack(ip.slicemaps[s].atlases), g[f"b{i}_int{s}"]), (i, s)
+            assert ip.thresholds[s] == inter["thresholds"][str(s)], (i, s)
+        assert list(ip.warnings) == inter["warnings"], i
+        # atlas files (slicemap.py:158-166): same manifest, pixels round-trip
+        mp = ops.save_slicemaps(dp.slicemaps, tmp_path / f"data{i}")
+        man = json.loads(mp.read_text())
+        assert man == dp.slicemaps.manifest()
+        for m, name in enumerate(man["atlases"]):
+            with Image.open(tmp_path / f"data{i}" / name) as im:
+                assert np.array_equal(np.asarray(im), g[f"b{i}_data"][m]), (i, name)
