@@ -301,6 +301,21 @@ def bundle_golden() -> None:
             for s in (128, 256, 512):
                 man = json.loads((bundle / "interactive" / str(s) / "manifest.json").read_text())
                 g[f"b{i}_int{s}"] = np.stack([png(f"interactive/{s}/{a}") for a in man["atlases"]])
+            if bid == "fixture-128":
+                # the viewer's reference frames (make-fixtures.py:99-130; frames/params.json): renders of
+                # the decoded interactive 128 scheme at the scheme's own threshold
+                from ctprev.render import ViewParams, render_view
+                from ctprev.slicemap import decode_slicemaps, load_slicemaps
+                frames_meta = json.loads((ref / "frontend/tests/fixtures/frames/params.json").read_text())
+                dec = decode_slicemaps(load_slicemaps(bundle / "interactive" / "128" / "manifest.json"))
+                imgs = []
+                for fr in frames_meta["frames"]:
+                    vp = ViewParams(azimuth_deg=fr["azimuth"], image_dim=frames_meta["image_dim"],
+                                    steps=frames_meta["steps"], mode=fr["mode"], threshold=fr["threshold"],
+                                    gain=frames_meta["gain"])
+                    imgs.append(render_view(dec, vp))
+                g["frames_params"] = np.array(json.dumps(frames_meta))
+                g["frames_img"] = np.stack(imgs)
     finally:
         shutil.rmtree(work, ignore_errors=True)
     out = Path(__file__).resolve().parent / "ref_golden_bundles.npz"

@@ -615,3 +615,17 @@ def test_bundles_pixel_parity(P, cuda, tmp_path):
         for m, name in enumerate(man["atlases"]):
             with Image.open(tmp_path / f"data{i}" / name) as im:
                 assert np.array_equal(np.asarray(im), g[f"b{i}_data"][m]), (i, name)
+
+
+def test_viewer_reference_frames(P, golden):
+    """frontend/tests/fixtures/frames/params.json: surface (3 azimuths) and additive
+    renders of the fixture bundle's decoded interactive-128 scheme -- bit-exact."""
+    import json
+    from pathlib import Path
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_bundles.npz") as z:
+        atl, fm, ref = z["b0_int128"], json.loads(str(z["frames_params"])), z["frames_img"]
+    vol = P.decode_slicemaps(P.SlicemapSet(scheme=P.plan_scheme(128), atlases=tuple(atl)))
+    for k, fr in enumerate(fm["frames"]):
+        vp = P.ViewParams(azimuth_deg=fr["azimuth"], image_dim=fm["image_dim"], steps=fm["steps"], mode=fr["mode"],
+                          threshold=fr["threshold"], gain=fm["gain"])
+        assert np.array_equal(P.render_view(vol, vp), ref[k]), fr["file"]

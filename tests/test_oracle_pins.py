@@ -210,3 +210,22 @@ def test_otsu_matches_reference_interactive_golden():
         for s in (128, 256, 512):
             t = O.otsu_threshold(g[f"ip{i}_hist{s}"])
             assert (-1 if t is None else t) == int(g[f"ip{i}_thr{s}"]), (i, s)
+
+
+def test_oracle_viewer_frames_and_bundle_products():
+    """The oracle on the recorded fixture bundle: decode the interactive-128 atlases and
+    render the viewer's reference frames (bit-exact); data-preview bins from the volume."""
+    import json
+    from pathlib import Path
+    with np.load(Path(__file__).resolve().parent / "golden" / "ref_golden_bundles.npz") as z:
+        atl, fm, ref = z["b0_int128"], json.loads(str(z["frames_params"])), z["frames_img"]
+        meta = json.loads(str(z["b0_meta"]))
+        vol = z["b0_vol"]
+        data = z["b0_data"]
+    cube = O.decode_slicemaps(list(atl), (128, 1024, 8, 2))
+    for k, fr in enumerate(fm["frames"]):
+        img = O.render_view(cube, fr["azimuth"], fm["image_dim"], fm["steps"], fr["mode"], fr["threshold"], fm["gain"])
+        assert np.array_equal(img, ref[k]), fr["file"]
+    bins, atl_dp = O.build_data_preview(vol)
+    assert sorted(bins) == meta["previews"]["data"]["filtered_bins"]
+    assert np.array_equal(np.stack(atl_dp), data)
