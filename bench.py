@@ -349,8 +349,23 @@ def main():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e_s = float(et.item())
         vox_e2e = sess.shape[0] * ny * nx * (world if world > 1 else 1)
+        # the PCIe bound of this path: a plain pinned H2D copy of the same 1 GiB
+        h2d = torch.empty(sess.shape, dtype=torch.uint8, device=device)
+        h2d.copy_(host, non_blocking=True)
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(3):
+            h2d.copy_(host, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = 3 * host.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del h2d
+        e_gbs = sess.h2d_bytes * e_steps / e_s / 1e9
         e2e = {"value": vox_e2e * e_steps / e_s / 1e9, "unit": "GVoxel/s",
                "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes, "steps": e_steps,
+               "h2d_GBps": e_gbs, "pcie_h2d_copy_GBps": h2d_gbs, "pcie_frac": e_gbs / h2d_gbs,
                "path": "PreviewSession.run(pinned host volume): z-chunk streamed H2D / fused pass / atlas D2H on "
                        "3 CUDA streams" + ("" if world == 1 else "; one scan per rank")}
         del sess, host
