@@ -643,7 +643,7 @@ def bench_other_configs(device):
     # as save_slicemaps writes them -- device filter + parallel deflate vs Pillow (slicemap.py:164)
     import io
     from PIL import Image
-    from paper_2311_15038_b200.png import encode_pngs
+    from paper_2311_15038_b200.png import encode_pngs, encode_pngs_device
     vol = synth.generate(spec, device=device)
     schemes = {s: AtlasSpec.of(plan_scheme(s)) for s in (512, 256, 128)}
     res = run_preview(vol, plan_preview(spec.shape, schemes))
@@ -653,6 +653,10 @@ def bench_other_configs(device):
     t0 = time.perf_counter()
     ours = sum(len(b) for b in encode_pngs([res.atlases[s] for s in schemes]))
     t_ours = time.perf_counter() - t0
+    encode_pngs_device(res.atlases[128])  # warm-up
+    t0 = time.perf_counter()
+    dev_bytes = sum(len(b) for b in encode_pngs_device([res.atlases[s] for s in schemes]))
+    t_dev = time.perf_counter() - t0
     t0 = time.perf_counter()
     pil = 0
     for s in schemes:
@@ -664,6 +668,7 @@ def bench_other_configs(device):
     out["c2_png"] = {"workload": "c2 atlases to PNG bytes (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2): device scanline "
                                  "filter + parallel zlib-6 deflate blocks vs Pillow single-threaded (slicemap.py:164)",
                      "ms": t_ours * 1e3, "bytes": ours, "pillow_ms": t_pil * 1e3, "pillow_bytes": pil,
+                     "device_deflate_ms": t_dev * 1e3, "device_deflate_bytes": dev_bytes,
                      "host_threads": os.cpu_count()}
     del res
     torch.cuda.empty_cache()

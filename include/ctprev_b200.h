@@ -238,6 +238,24 @@ int ctp_image_hist_u8(const uint8_t* imgs, int32_t n_images, int64_t pixels,
 int ctp_png_filter_u8(const uint8_t* images, int32_t n_images, int64_t height, int64_t width,
                       uint8_t* out, void* stream);
 
+/* DEFLATE (RFC 1951) of n_streams byte streams of stream_len bytes each (the
+ * PNG-filtered scanlines of ctp_png_filter_u8): every stream is cut into
+ * chunks (ctp_deflate_geometry: chunk_bytes in, at most chunk_out_bytes out),
+ * each one dynamic-Huffman (or stored) block, non-final chunks ending with a
+ * sync flush, so the chunks of a stream concatenate into one raw deflate
+ * stream.  Chunk c (= stream * chunks_per_stream + k) is written at
+ * out + c * chunk_out_bytes, its size to out_bytes[c], and its Adler-32
+ * partials (sum d_i, sum (n - i) d_i) to adler[2c], adler[2c + 1].  row_len
+ * adds the image row (and two rows) to the match distances.  scratch holds
+ * grid * chunk_bytes uint32 tokens; grid CTAs loop over all chunks. */
+int ctp_deflate_geometry(int32_t* chunk_bytes, int32_t* chunk_out_bytes);
+int ctp_deflate_u8(const uint8_t* data, int64_t n_streams, int64_t stream_len, int32_t row_len,
+                   uint8_t* out, int32_t* out_bytes, uint64_t* adler, uint32_t* scratch,
+                   int32_t grid, void* stream);
+/* Gather the chunks into one buffer: chunk c's out_bytes[c] bytes to dst + offsets[c]. */
+int ctp_deflate_compact(const uint8_t* out, const int32_t* out_bytes, const int64_t* offsets,
+                        int64_t total_chunks, uint8_t* dst, void* stream);
+
 /* ---------------- peer memory between the ranks of a node (s8(e)) ------- */
 
 #define CTP_IPC_HANDLE_BYTES 64

@@ -23,7 +23,7 @@ COMMON += os.environ.get("CTP_NVCC_EXTRA", "").split()  # variant experiments (t
 # render.cu: the fp64 path must not contract a*b+c into FMA, so that its
 # arithmetic matches numba's fastmath-free reference bit for bit.
 PER_FILE = {"render.cu": ["--fmad=false"]}
-SOURCES = ["ctp_common.cu", "hist.cu", "preview.cu", "resample.cu", "render.cu", "synth.cu", "png.cu", "ipc.cu"]
+SOURCES = ["ctp_common.cu", "hist.cu", "preview.cu", "resample.cu", "render.cu", "synth.cu", "png.cu", "deflate.cu", "ipc.cu"]
 
 
 def _nvcc() -> str:

@@ -1,5 +1,8 @@
 """Atlas PNG writing: ``save_slicemaps`` (slicemap.py:158-166).
 
+Two compressors after the device scanline filter: parallel host zlib blocks
+(default) or the device deflate of csrc/deflate.cu (``compressor="device"``).
+
 The reference writes every atlas with ``Image.fromarray(atlas, "L").save(...)``:
 one thread filters and deflates 16 MB per 4096^2 atlas.  Here the PNG scanline
 filter (adaptive per row, ``ctp_png_filter_u8``) runs on the device over all
@@ -35,8 +38,20 @@ def _pool() -> ThreadPoolExecutor:
     return _POOL
 
 
-def _chunk(tag: bytes, data: bytes) -> bytes:
-    return struct.pack(">I", len(data)) + tag + data + struct.pack(">I", zlib.crc32(tag + data) & 0xFFFFFFFF)
+def _chunk(tag: bytes, data) -> bytes:
+    return struct.pack(">I", len(data)) + tag + bytes(data) + struct.pack(">I", zlib.crc32(data, zlib.crc32(tag)) & 0xFFFFFFFF)
+
+
+_IDAT_PIECE = 1 << 20
+
+
+def _idat_chunks(z) -> bytes:
+    """The zlib stream as IDAT chunks of <= 1 MiB (PNG allows any split), their CRCs
+    computed in parallel on the host pool (zlib releases the GIL)."""
+    mv = memoryview(z)
+    pieces = [mv[a:a + _IDAT_PIECE] for a in range(0, len(mv), _IDAT_PIECE)] or [mv[0:0]]
+    crcs = list(_pool().map(lambda p: zlib.crc32(p, zlib.crc32(b"IDAT")) & 0xFFFFFFFF, pieces))
+    return b"".join(struct.pack(">I", len(p)) + b"IDAT" + p + struct.pack(">I", c) for p, c in zip(pieces, crcs))
 
 
 def _deflate_block(mv, level: int, last: bool) -> bytes:
@@ -83,12 +98,93 @@ def encode_pngs(images, level: int = 6, block_rows: int = 256) -> list[bytes]:
     return [_assemble(*j) for j in jobs]
 
 
-def save_slicemaps(sset, out_dir, level: int = 6) -> Path:
-    """slicemap.py:158-166: atlases as PNG (``sm_<s>_<i>.png``) + ``manifest.json``."""
+MOD_ADLER = 65521
+_PINNED: torch.Tensor | None = None  # reused pinned staging buffer for the compressed bytes
+
+
+def deflate_device(filt: torch.Tensor) -> list[bytes]:
+    """zlib streams of the filtered scanlines (n, H, W + 1) of n images, compressed on the
+    device (``ctp_deflate_u8``: 16 KiB chunks, dynamic Huffman, sync-flush seams); the
+    host only concatenates chunks and combines the per-chunk Adler-32 partials."""
+    import ctypes as C
+    from . import _lib
+    from . import device as dev
+    n, h, w1 = filt.shape
+    L = h * w1
+    cb, ob = C.c_int32(), C.c_int32()
+    _lib.call("ctp_deflate_geometry", C.byref(cb), C.byref(ob))
+    chunk, slot = cb.value, ob.value
+    cps = -(-L // chunk)
+    total = n * cps
+    grid = 3 * torch.cuda.get_device_properties(filt.device).multi_processor_count
+    out = torch.empty(total * slot, dtype=torch.uint8, device=filt.device)
+    sizes = torch.empty(total, dtype=torch.int32, device=filt.device)
+    adler = torch.empty(2 * total, dtype=torch.int64, device=filt.device)
+    scratch = torch.empty(min(grid, total) * chunk, dtype=torch.int32, device=filt.device)
+    _lib.call("ctp_deflate_u8", dev._ptr(filt), n, L, w1, dev._ptr(out), dev._ptr(sizes), dev._ptr(adler),
+              dev._ptr(scratch), grid, dev._stream())
+    # one contiguous buffer of all chunks (device gather), then one pinned D2H
+    ends = torch.cumsum(sizes.to(torch.int64), 0)
+    offsets = ends - sizes.to(torch.int64)
+    nbytes = int(ends[-1].item())
+    packed = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=filt.device)
+    _lib.call("ctp_deflate_compact", dev._ptr(out), dev._ptr(sizes), dev._ptr(offsets), total, dev._ptr(packed),
+              dev._stream())
+    global _PINNED
+    if _PINNED is None or _PINNED.numel() < nbytes:
+        _PINNED = torch.empty(max(nbytes, 1 << 24), dtype=torch.uint8, pin_memory=True)
+    host = _PINNED[:nbytes]
+    host.copy_(packed[:nbytes])
+    body = memoryview(host.numpy())
+    off = offsets.cpu().numpy()
+    sz = sizes.cpu().numpy().astype(np.int64)
+    ad = adler.cpu().numpy().view(np.uint64).reshape(n, cps, 2).astype(object)
+    nk = np.minimum(chunk, L - np.arange(cps) * chunk)
+    rest = (L - np.arange(cps) * chunk - nk).astype(object)  # bytes after each chunk: weight of its sum in B
+    res = []
+    for i in range(n):
+        s1, s2 = ad[i, :, 0], ad[i, :, 1]
+        A = (1 + int(s1.sum())) % MOD_ADLER
+        B = (L + int((s1 * rest).sum()) + int(s2.sum())) % MOD_ADLER
+        a0, a1 = int(off[i * cps]), int(off[i * cps + cps - 1] + sz[i * cps + cps - 1])
+        res.append(b"".join((b"\x78\x9c", body[a0:a1], struct.pack(">I", (B << 16) | A))))
+    return res
+
+
+def png_from_zlib(z, width: int, height: int) -> bytes:
+    ihdr = struct.pack(">IIBBBBB", width, height, 8, 0, 0, 0, 0)
+    return _SIG + _chunk(b"IHDR", ihdr) + _idat_chunks(z) + _chunk(b"IEND", b"")
+
+
+def encode_pngs_device(images) -> list[bytes]:
+    """PNG bytes with filtering AND compression on the device (see ``deflate_device``)."""
+    from . import device as dev
+    stacks = images if isinstance(images, (list, tuple)) else [images]
+    res = []
+    for st in stacks:
+        t = st if isinstance(st, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(st))
+        if not t.is_cuda:
+            t = t.to("cuda", non_blocking=False)
+        filt = dev.png_filter(t.contiguous())
+        n, h, w1 = filt.shape
+        res += [png_from_zlib(z, w1 - 1, h) for z in deflate_device(filt)]
+    return res
+
+
+def save_slicemaps(sset, out_dir, level: int = 6, compressor: str = "zlib") -> Path:
+    """slicemap.py:158-166: atlases as PNG (``sm_<s>_<i>.png``) + ``manifest.json``.
+    ``compressor``: "zlib" (device filter + parallel host zlib at ``level``, files
+    within 10% of Pillow's) or "device" (filter and deflate on the GPU: ~7x faster
+    again, files ~20% larger)."""
     out_dir = Path(out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
     names = sset.scheme.atlas_names()
-    pngs = encode_pngs(np.stack(sset.atlases), level)
+    if compressor == "device":
+        pngs = encode_pngs_device(np.stack(sset.atlases))
+    elif compressor == "zlib":
+        pngs = encode_pngs(np.stack(sset.atlases), level)
+    else:
+        raise ValueError(f"compressor {compressor!r}: expected 'zlib' or 'device'")
     for name, data in zip(names, pngs):
         (out_dir / name).write_bytes(data)
     manifest_path = out_dir / "manifest.json"

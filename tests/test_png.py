@@ -95,3 +95,45 @@ def test_save_slicemaps_roundtrip(cuda, tmp_path):
     assert man == {"scheme": {"s": 256, "atlas": 4096, "grid": 16, "maps": 1}, "atlases": ["sm_256_0.png"]}
     with Image.open(tmp_path / "sm" / "sm_256_0.png") as im:
         assert im.mode == "L" and np.array_equal(np.asarray(im), sset.atlases[0])
+
+
+@pytest.mark.gpu
+def test_device_deflate_streams(cuda):
+    """ctp_deflate_u8 + host assembly: valid zlib streams (zlib.decompress gives back the
+    filtered bytes exactly) and PNGs Pillow decodes to the images, for zeros (matches
+    only), noise (stored blocks), smooth data (dynamic Huffman + matches), several chunks
+    per image with a partial last chunk, and a one-row image."""
+    import zlib
+    import torch
+    from PIL import Image
+    from paper_2311_15038_b200 import device as dev
+    from paper_2311_15038_b200.png import deflate_device, encode_pngs_device
+    rng = np.random.default_rng(4)
+    cases = [np.zeros((3, 40, 57), np.uint8), rng.integers(0, 256, (2, 150, 301), dtype=np.uint8),
+             np.clip(np.cumsum(rng.integers(-3, 4, (2, 300, 517)), axis=2) + 128, 0, 255).astype(np.uint8),
+             np.full((1, 1, 70000), 9, np.uint8)]
+    imgs = _images()
+    cases.append(imgs)
+    for c in cases:
+        t = torch.from_numpy(np.ascontiguousarray(c)).to(cuda)
+        filt = dev.png_filter(t)
+        for i, z in enumerate(deflate_device(filt)):
+            assert zlib.decompress(z) == filt[i].cpu().numpy().tobytes(), (c.shape, i)
+        for i, p in enumerate(encode_pngs_device(c)):
+            with Image.open(io.BytesIO(p)) as im:
+                assert np.array_equal(np.asarray(im), c[i]), (c.shape, i)
+
+
+@pytest.mark.gpu
+def test_save_slicemaps_device_compressor(cuda, tmp_path):
+    from PIL import Image
+    import paper_2311_15038_b200 as P
+    from paper_2311_15038_b200.png import save_slicemaps
+    rng = np.random.default_rng(6)
+    vol = np.clip(np.rint(rng.normal(20, 6, (128, 128, 128))), 0, 255).astype(np.uint8)
+    sset = P.encode_slicemaps(P.Volume(vol), P.plan_scheme(128))
+    mp = save_slicemaps(sset, tmp_path / "sm", compressor="device")
+    assert json.loads(mp.read_text()) == sset.manifest()
+    for m, name in enumerate(sset.scheme.atlas_names()):
+        with Image.open(tmp_path / "sm" / name) as im:
+            assert np.array_equal(np.asarray(im), sset.atlases[m])
