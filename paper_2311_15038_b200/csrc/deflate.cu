@@ -75,6 +75,8 @@ struct DeflateSmem {
   uint32_t warp_bits[kDThreads / 32];
   uint32_t end_bits;
   unsigned long long red[kDThreads / 32][2];
+  uint32_t bhist[256];        // byte histogram of the chunk
+  uint8_t litcost[256];       // estimated literal cost, quarter bits: -4 log2(p)
   uint8_t lsym_tab[259];      // match length -> length symbol - 257
   uint8_t dsym_tab[512];      // distance -> distance symbol (zlib's split table)
   uint16_t rank[286];
@@ -100,11 +102,19 @@ __device__ __forceinline__ void put_bits(uint32_t* w, uint32_t pos, uint32_t val
 // (frequencies, bit counts, bit writing) instead of storing tokens: returns
 // the token at position i (literal: value < 256; match: flag | length symbol
 // | length extra | distance symbol | distance extra) and advances i.
+// A match is taken only when its estimated cost (length and distance codes of
+// ~7 and ~5 bits plus their extra bits) is below the estimated cost of its
+// bytes as literals (-log2 of their frequency in the chunk): on noise, short
+// coincidental matches cost more than Huffman-coded literals.
 __device__ __forceinline__ uint32_t next_token(const DeflateSmem& S, const int* cand_d, int& i, int end) {
   const int L = min((int)S.best_len[i], end - i);
   if (L >= 3) {
     const int d = cand_d[S.best_c[i]];
     const int ls = S.lsym_tab[L], ds = dsym_of(S, d);
+    int lit = 0;
+    for (int q = 0; q < L; q++) lit += S.litcost[S.buf[i + q]];
+    const int mcost = 4 * (7 + c_len_extra[ls] + 5 + c_dist_extra[ds]);
+    if (mcost >= lit) return S.buf[i++];
     i += L;
     return 0x80000000u | ((uint32_t)ls << 23) | ((uint32_t)(L - c_len_base[ls]) << 18) | ((uint32_t)ds << 13) |
            (uint32_t)(d - c_dist_base[ds]);
@@ -241,6 +251,18 @@ __global__ void __launch_bounds__(kDThreads) deflate_kernel(const DeflateArgs a)
       a.adler[2 * c] = t1;
       a.adler[2 * c + 1] = t2;
     }
+
+    // ---- literal cost estimates from the chunk's byte histogram
+    for (int i = tid; i < 256; i += kDThreads) S.bhist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kDThreads) atomicAdd(&S.bhist[S.buf[i]], 1u);
+    __syncthreads();
+    for (int b = tid; b < 256; b += kDThreads) {
+      const uint32_t h = S.bhist[b];
+      const float bits = h ? __log2f((float)n / (float)h) : 15.f;
+      S.litcost[b] = (uint8_t)min(60, max(1, __float2int_rn(4.f * bits)));
+    }
+    __syncthreads();
 
     // ---- matches within the own segment, then the greedy parse of it
     const int p0 = tid * kDSeg, p1 = min(n, p0 + kDSeg);
