@@ -23,6 +23,13 @@
 // A persistent grid loops over all chunks of all images.
 #include "ctp_common.cuh"
 
+#ifndef CTP_DEFL_LBITS
+#define CTP_DEFL_LBITS 1  // length-code bits charged to a match when deciding it (tuned on the c2 atlases)
+#endif
+#ifndef CTP_DEFL_DBITS
+#define CTP_DEFL_DBITS 1  // distance-code bits charged (1 + 1: 44.2 MB; the code-length estimate 7 + 5: 46.5 MB)
+#endif
+
 namespace ctp {
 
 constexpr int kDChunk = 16384;                  // bytes per chunk (one block)
@@ -102,10 +109,11 @@ __device__ __forceinline__ void put_bits(uint32_t* w, uint32_t pos, uint32_t val
 // (frequencies, bit counts, bit writing) instead of storing tokens: returns
 // the token at position i (literal: value < 256; match: flag | length symbol
 // | length extra | distance symbol | distance extra) and advances i.
-// A match is taken only when its estimated cost (length and distance codes of
-// ~7 and ~5 bits plus their extra bits) is below the estimated cost of its
-// bytes as literals (-log2 of their frequency in the chunk): on noise, short
-// coincidental matches cost more than Huffman-coded literals.
+// A match is taken only when a charged cost (CTP_DEFL_LBITS + CTP_DEFL_DBITS
+// plus the extra bits) is below the estimated cost of its bytes as literals
+// (-log2 of their frequency in the chunk): matches of bytes that are nearly
+// free as literals are skipped, and the parse re-tries one byte later (a cheap
+// form of lazy matching).
 __device__ __forceinline__ uint32_t next_token(const DeflateSmem& S, const int* cand_d, int& i, int end) {
   const int L = min((int)S.best_len[i], end - i);
   if (L >= 3) {
@@ -113,7 +121,7 @@ __device__ __forceinline__ uint32_t next_token(const DeflateSmem& S, const int* 
     const int ls = S.lsym_tab[L], ds = dsym_of(S, d);
     int lit = 0;
     for (int q = 0; q < L; q++) lit += S.litcost[S.buf[i + q]];
-    const int mcost = 4 * (7 + c_len_extra[ls] + 5 + c_dist_extra[ds]);
+    const int mcost = 4 * (CTP_DEFL_LBITS + c_len_extra[ls] + CTP_DEFL_DBITS + c_dist_extra[ds]);
     if (mcost >= lit) return S.buf[i++];
     i += L;
     return 0x80000000u | ((uint32_t)ls << 23) | ((uint32_t)(L - c_len_base[ls]) << 18) | ((uint32_t)ds << 13) |
