@@ -174,14 +174,67 @@ __device__ __forceinline__ bool in_circle(int64_t x, int64_t y, double cx, doubl
   return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= r2;
 }
 
-__global__ void circle_mask_kernel(const uint8_t* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, double cx,
-                                   double cy, double r2, uint8_t* __restrict__ out) {
-  const int64_t total = nz * ny * nx;
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t x = o % nx;
-    const int64_t y = (o / nx) % ny;
-    out[o] = in_circle(x, y, cx, cy, r2) ? __ldg(in + o) : (uint8_t)0;
+// The kept set of row y is an interval [xa, xb] of x: the fp64 predicate is
+// monotone in |fl(x - cx)| (every rounding step is monotone), so it holds on
+// the integers around the one nearest cx and fails beyond two boundaries,
+// found by binary search with the exact predicate (row_span_kernel, one thread
+// per row y); every slice then applies the same spans with 16-byte copies.
+__global__ void circle_span_kernel(int64_t ny, int64_t nx, double cx, double cy, double r2, int2* __restrict__ span) {
+  const int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (y >= ny) return;
+  int64_t xc = (int64_t)floor(cx + 0.5);
+  if (xc > nx - 1) xc = nx - 1;
+  if (xc < 0) xc = 0;
+  if (xc + 1 <= nx - 1 && !in_circle(xc, y, cx, cy, r2) && in_circle(xc + 1, y, cx, cy, r2)) xc++;
+  if (!in_circle(xc, y, cx, cy, r2)) {
+    span[y] = make_int2(1, 0);  // empty
+    return;
   }
+  int64_t lo = 0, hi = xc;  // smallest x in [0, xc] inside
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (in_circle(mid, y, cx, cy, r2)) hi = mid; else lo = mid + 1;
+  }
+  const int64_t xa = lo;
+  lo = xc;
+  hi = nx - 1;  // largest x in [xc, nx - 1] inside
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (in_circle(mid, y, cx, cy, r2)) lo = mid; else hi = mid - 1;
+  }
+  span[y] = make_int2((int)xa, (int)lo);
+}
+
+// keep [xa, xb] of every row, zero the rest: one 16-byte chunk per thread
+// (grid-stride) when rows are 16-byte granular, else one CTA per row, bytewise
+__global__ void __launch_bounds__(256) circle_apply_vec_kernel(const uint8_t* __restrict__ in, uint32_t ny,
+                                                               uint32_t nc, uint32_t total, const int2* __restrict__ span,
+                                                               uint8_t* __restrict__ out) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < total; c += gridDim.x * blockDim.x) {
+    const uint32_t row = c / nc, x = (c - row * nc) * 16;
+    const int2 sp = span[row % ny];
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if ((int)x >= sp.x && (int)x + 15 <= sp.y) {
+      v = __ldg(reinterpret_cast<const uint4*>(in) + c);
+    } else if ((int)x + 15 >= sp.x && (int)x <= sp.y) {  // a boundary chunk
+      uint8_t b[16];
+      *reinterpret_cast<uint4*>(b) = __ldg(reinterpret_cast<const uint4*>(in) + c);
+#pragma unroll
+      for (int q = 0; q < 16; q++)
+        if ((int)x + q < sp.x || (int)x + q > sp.y) b[q] = 0;
+      v = *reinterpret_cast<uint4*>(b);
+    }
+    reinterpret_cast<uint4*>(out)[c] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) circle_apply_kernel(const uint8_t* __restrict__ in, int64_t ny, int64_t nx,
+                                                           const int2* __restrict__ span, uint8_t* __restrict__ out) {
+  const int64_t row = blockIdx.x;  // z * ny + y
+  const int2 sp = span[row % ny];
+  const uint8_t* src = in + row * nx;
+  uint8_t* dst = out + row * nx;
+  for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) dst[x] = (x >= sp.x && x <= sp.y) ? __ldg(src + x) : 0;
 }
 
 static int grid1d(int64_t n, int threads) {
@@ -257,9 +310,23 @@ int ctp_circle_mask_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, do
   // mask.py:202-205 (the radius / margin checks stay with the caller, which holds the Circle)
   CTP_REQUIRE(0.0 <= cx && cx < (double)nx && 0.0 <= cy && cy < (double)ny, CTP_E_INVALID,
               "center (%.1f, %.1f) outside %lldx%lld slice", cx, cy, (long long)nx, (long long)ny);
-  const int64_t total = nx * ny * nz;
-  circle_mask_kernel<<<grid1d(total, 256), 256, 0, as_stream(stream)>>>(in, nz, ny, nx, cx, cy, r_eff_sq, out);
-  CTP_CUDA_CHECK_LAUNCH("circle_mask_kernel");
+  CTP_REQUIRE(nx < (1LL << 31) && ny * nz < (1LL << 31), CTP_E_INVALID, "ctp_circle_mask_u8: shape too large");
+  cudaStream_t st = as_stream(stream);
+  int2* span = nullptr;
+  CTP_CUDA_CALL(cudaMallocAsync(&span, (size_t)ny * sizeof(int2), st));
+  circle_span_kernel<<<(unsigned)((ny + 127) / 128), 128, 0, st>>>(ny, nx, cx, cy, r_eff_sq, span);
+  CTP_CUDA_CHECK_LAUNCH("circle_span_kernel");
+  const int64_t chunks = nx / 16 * ny * nz;
+  if ((nx & 15) == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0 &&
+      chunks < (1LL << 32)) {
+    circle_apply_vec_kernel<<<grid1d(chunks, 256), 256, 0, st>>>(in, (uint32_t)ny, (uint32_t)(nx / 16),
+                                                                  (uint32_t)chunks, span, out);
+    CTP_CUDA_CHECK_LAUNCH("circle_apply_vec_kernel");
+  } else {
+    circle_apply_kernel<<<(unsigned)(ny * nz), 256, 0, st>>>(in, ny, nx, span, out);
+    CTP_CUDA_CHECK_LAUNCH("circle_apply_kernel");
+  }
+  CTP_CUDA_CALL(cudaFreeAsync(span, st));
   return CTP_OK;
 }
 

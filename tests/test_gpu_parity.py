@@ -629,3 +629,22 @@ def test_viewer_reference_frames(P, golden):
         vp = P.ViewParams(azimuth_deg=fr["azimuth"], image_dim=fm["image_dim"], steps=fm["steps"], mode=fr["mode"],
                           threshold=fr["threshold"], gain=fm["gain"])
         assert np.array_equal(P.render_view(vol, vp), ref[k]), fr["file"]
+
+
+def test_circle_mask_spans_random(P, cuda):
+    """The span form of the mask (binary search of the exact fp64 predicate per row,
+    16-byte copies) equals the oracle per voxel: random circles, centres on and off
+    the grid, radii whose boundary passes exactly through lattice points, widths on
+    and off the 16-byte path, circles larger than the slice."""
+    rng = np.random.default_rng(12)
+    cases = [((3, 50, 64), 31.5, 24.5, 20.0, 0.0), ((2, 64, 80), 40.0, 30.0, 5.0 / 0.98, 0.02),  # 3-4-5 boundary
+             ((2, 37, 53), 0.0, 0.0, 30.0, 0.1), ((2, 48, 48), 47.9, 47.9, 100.0, 0.0), ((1, 33, 96), 50.2, 16.7, 0.3, 0.0)]
+    for _ in range(6):
+        nz, ny, nx = int(rng.integers(1, 4)), int(rng.integers(8, 90)), int(rng.choice([16, 48, 64, 70, 128, 131]))
+        cases.append(((nz, ny, nx), float(rng.uniform(0, nx)), float(rng.uniform(0, ny)), float(rng.uniform(1, 80)),
+                      float(rng.choice([0.0, 0.02, 0.3]))))
+    from types import SimpleNamespace as C
+    for shape, cx, cy, r, m in cases:
+        v = rng.integers(1, 256, size=shape, dtype=np.uint8)
+        got = P.apply_circle_mask(P.Volume(v), C(cx=cx, cy=cy, r=r), margin=m).voxels
+        assert np.array_equal(got, O.apply_circle_mask(v, cx, cy, r, m)), (shape, cx, cy, r, m)
