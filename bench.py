@@ -548,130 +548,151 @@ def bench_other_configs(device):
     from paper_2311_15038_b200.types import ViewParams, plan_scheme
     peak = _peaks()[0]["hbm_gbs"]
     out = {}
-    # c1
-    spec = synth.config("c1")
-    vol = synth.generate(spec, device=device)
-    plan = plan_preview(spec.shape, {256: AtlasSpec(256, 4096, 16, 1)})
-    res = run_preview(vol, plan)
-    ms_eager = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 200)
-    # the step is launch-bound at this size: replay it as a CUDA graph (one cooperative kernel node)
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        for _ in range(3):
+    def _c1():
+        # c1
+        spec = synth.config("c1")
+        vol = synth.generate(spec, device=device)
+        plan = plan_preview(spec.shape, {256: AtlasSpec(256, 4096, 16, 1)})
+        res = run_preview(vol, plan)
+        ms_eager = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 200)
+        # the step is launch-bound at this size: replay it as a CUDA graph (one cooperative kernel node)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                run_preview(vol, plan, hist=res.hist)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
             run_preview(vol, plan, hist=res.hist)
-    torch.cuda.current_stream().wait_stream(side)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        run_preview(vol, plan, hist=res.hist)
-    ms = _time_steps(graph.replay, 200)
-    n = vol.numel()
-    out["c1"] = {"workload": "256^3 u8: hist + artifact-bin filter + one 16x16-grid 4096^2 atlas", "ms_per_step": ms,
-                 "ms_per_step_eager": ms_eager, "gvoxel_per_s": n / ms / 1e6, "alg_bytes": 2 * n,
-                 "frac_of_hbm_peak": 2 * n / (ms * 1e-3) / 1e9 / peak,
-                 "note": "32 MB working set: launch/L2-bound (SURVEY s8 d); one cooperative launch per step, "
-                         "replayed from a CUDA graph"}
-    del graph
-    del vol, res
-    # c3
-    spec = synth.config("c3")
-    vol = synth.generate(spec, device=device)
-    schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec.of(plan_scheme(512)),
-               256: AtlasSpec.of(plan_scheme(256)), 128: AtlasSpec.of(plan_scheme(128))}
-    plan = plan_preview(spec.shape, schemes)
-    res = run_preview(vol, plan)
-    ms = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 10)
-    n = vol.numel()
-    alg = 2 * n + sum(t.numel() for t in res.atlases.values())
-    out["c3"] = {"workload": "2048^3 12-bit u16 (16 GiB): 4096-bin hist + filter o rescale + 4-level pyramid + atlases "
-                             "(1024: 64 maps of 4x4 4096^2; 512/256/128 planned)", "ms_per_step": ms,
-                 "gvoxel_per_s": n / ms / 1e6, "alg_bytes": alg, "achieved_GBps": alg / (ms * 1e-3) / 1e9,
-                 "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak}
-    del vol, res
-    torch.cuda.empty_cache()
-    # c4 alpha
-    spec = synth.config("c4")
-    vol = synth.generate(spec, device=device)
-    steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * spec.shape[0])
-    views = [ViewParams(azimuth_deg=10.0 * k, image_dim=1024, steps=steps, mode="alpha") for k in range(36)]
-    img = dev.render(vol, views, channels=4, fp32=True)
-    ms = _time_steps(lambda: dev.render(vol, views, channels=4, fp32=True, out=img), 2, warmup=1)
-    out["c4_alpha"] = {"workload": "36 azimuths x 1024^2 RGBA8, front-to-back alpha, 4-point TF, early stop 0.99, "
-                                   f"{steps} steps", "frames_per_s": 36 / (ms * 1e-3), "ms_per_frame": ms / 36}
-    del vol, img
-    torch.cuda.empty_cache()
-    # c5: stream of 1536^2 x 2048 u16 volumes, one GPU (replicas across GPUs)
-    from paper_2311_15038_b200.stream import PreviewStream
-    spec = synth.config("c5", seed=0)
-    vol = synth.generate(spec, device=device)
-    ps = PreviewStream(spec.shape, torch.uint16, device=device)
-    ms = _time_steps(lambda: ps.process(vol), 4, warmup=1)
-    n = vol.numel()
-    out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume: hist + filter o rescale + L1..L4 padded "
-                             "atlases + 36-view 512^2 MIP strip (from L2), one volume per GPU",
-                 "ms_per_volume": ms, "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6}
-    del vol, ps
-    torch.cuda.empty_cache()
-    # ingest: config 2 from ctprev's raw + JSON format, streamed from a file (page cache hot) through
-    # pinned chunks into the fused pass; the file is written to a temp dir here
-    import tempfile
-    from paper_2311_15038_b200.ingest import preview_from_raw
-    spec = synth.config("c2")
-    vol = synth.generate(spec, device=device)
-    with tempfile.TemporaryDirectory() as td:
-        nz, ny, nx = spec.shape
-        vol.cpu().numpy().tofile(os.path.join(td, "c2.raw"))
-        with open(os.path.join(td, "c2.json"), "w") as f:
-            json.dump({"dims": [nx, ny, nz], "dtype": "u8", "order": "xyz", "voxel_size_um": None}, f)
+        ms = _time_steps(graph.replay, 200)
+        n = vol.numel()
+        out["c1"] = {"workload": "256^3 u8: hist + artifact-bin filter + one 16x16-grid 4096^2 atlas", "ms_per_step": ms,
+                     "ms_per_step_eager": ms_eager, "gvoxel_per_s": n / ms / 1e6, "alg_bytes": 2 * n,
+                     "frac_of_hbm_peak": 2 * n / (ms * 1e-3) / 1e9 / peak,
+                     "note": "32 MB working set: launch/L2-bound (SURVEY s8 d); one cooperative launch per step, "
+                             "replayed from a CUDA graph"}
+        del graph
+        del vol, res
+
+    def _c3():
+        # c3
+        spec = synth.config("c3")
+        vol = synth.generate(spec, device=device)
+        schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec.of(plan_scheme(512)),
+                   256: AtlasSpec.of(plan_scheme(256)), 128: AtlasSpec.of(plan_scheme(128))}
+        plan = plan_preview(spec.shape, schemes)
+        res = run_preview(vol, plan)
+        ms = _time_steps(lambda: run_preview(vol, plan, hist=res.hist), 10)
+        n = vol.numel()
+        alg = 2 * n + sum(t.numel() for t in res.atlases.values())
+        out["c3"] = {"workload": "2048^3 12-bit u16 (16 GiB): 4096-bin hist + filter o rescale + 4-level pyramid + atlases "
+                                 "(1024: 64 maps of 4x4 4096^2; 512/256/128 planned)", "ms_per_step": ms,
+                     "gvoxel_per_s": n / ms / 1e6, "alg_bytes": alg, "achieved_GBps": alg / (ms * 1e-3) / 1e9,
+                     "frac_of_hbm_peak": alg / (ms * 1e-3) / 1e9 / peak}
+        del vol, res
+        torch.cuda.empty_cache()
+
+    def _c4_alpha():
+        # c4 alpha
+        spec = synth.config("c4")
+        vol = synth.generate(spec, device=device)
+        steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * spec.shape[0])
+        views = [ViewParams(azimuth_deg=10.0 * k, image_dim=1024, steps=steps, mode="alpha") for k in range(36)]
+        img = dev.render(vol, views, channels=4, fp32=True)
+        ms = _time_steps(lambda: dev.render(vol, views, channels=4, fp32=True, out=img), 2, warmup=1)
+        out["c4_alpha"] = {"workload": "36 azimuths x 1024^2 RGBA8, front-to-back alpha, 4-point TF, early stop 0.99, "
+                                       f"{steps} steps", "frames_per_s": 36 / (ms * 1e-3), "ms_per_frame": ms / 36}
+        del vol, img
+        torch.cuda.empty_cache()
+
+    def _c5():
+        # c5: stream of 1536^2 x 2048 u16 volumes, one GPU (replicas across GPUs)
+        from paper_2311_15038_b200.stream import PreviewStream
+        spec = synth.config("c5", seed=0)
+        vol = synth.generate(spec, device=device)
+        ps = PreviewStream(spec.shape, torch.uint16, device=device)
+        ms = _time_steps(lambda: ps.process(vol), 4, warmup=1)
+        n = vol.numel()
+        out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume: hist + filter o rescale + L1..L4 padded "
+                                 "atlases + 36-view 512^2 MIP strip (from L2), one volume per GPU",
+                     "ms_per_volume": ms, "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6}
+        del vol, ps
+        torch.cuda.empty_cache()
+
+    def _c2_ingest():
+        # ingest: config 2 from ctprev's raw + JSON format, streamed from a file (page cache hot) through
+        # pinned chunks into the fused pass; the file is written to a temp dir here
+        import tempfile
+        from paper_2311_15038_b200.ingest import preview_from_raw
+        spec = synth.config("c2")
+        vol = synth.generate(spec, device=device)
+        with tempfile.TemporaryDirectory() as td:
+            nz, ny, nx = spec.shape
+            vol.cpu().numpy().tofile(os.path.join(td, "c2.raw"))
+            with open(os.path.join(td, "c2.json"), "w") as f:
+                json.dump({"dims": [nx, ny, nz], "dtype": "u8", "order": "xyz", "voxel_size_um": None}, f)
+            del vol
+            from paper_2311_15038_b200.device import AtlasSpec as _AS
+            from paper_2311_15038_b200.pipeline import PreviewSession
+            sess = PreviewSession(spec.shape, torch.uint8, {s: _AS.of(plan_scheme(s)) for s in (512, 256, 128)})
+            preview_from_raw(os.path.join(td, "c2.json"), session=sess)  # warm-up (+ page cache)
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                preview_from_raw(os.path.join(td, "c2.json"), session=sess)
+                ts.append(time.perf_counter() - t0)
+            del sess
+            out["c2_ingest"] = {"workload": "c2 from <name>.raw + <name>.json (volume.py:205-249 format): header check, "
+                                            "64-slice pinned chunks read from the file (page cache hot, 8 preadv threads) "
+                                            "overlapped with H2D + fused pass, atlases back to host (session reused)",
+                                "ms_per_volume": min(ts) * 1e3, "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9,
+                                "host_bytes_held": 3 * 64 * ny * nx + 3 * ny * nx}
+
+    def _c2_png():
+        # atlas PNG writing: the c2 step's 14 atlases (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2)
+        # as save_slicemaps writes them -- device filter + parallel deflate vs Pillow (slicemap.py:164)
+        import io
+        from PIL import Image
+        from paper_2311_15038_b200.png import encode_pngs, encode_pngs_device
+        spec = synth.config("c2")
+        vol = synth.generate(spec, device=device)
+        schemes = {s: AtlasSpec.of(plan_scheme(s)) for s in (512, 256, 128)}
+        res = run_preview(vol, plan_preview(spec.shape, schemes))
         del vol
-        from paper_2311_15038_b200.device import AtlasSpec as _AS
-        from paper_2311_15038_b200.pipeline import PreviewSession
-        sess = PreviewSession(spec.shape, torch.uint8, {s: _AS.of(plan_scheme(s)) for s in (512, 256, 128)})
-        preview_from_raw(os.path.join(td, "c2.json"), session=sess)  # warm-up (+ page cache)
-        ts = []
-        for _ in range(3):
-            t0 = time.perf_counter()
-            preview_from_raw(os.path.join(td, "c2.json"), session=sess)
-            ts.append(time.perf_counter() - t0)
-        del sess
-        out["c2_ingest"] = {"workload": "c2 from <name>.raw + <name>.json (volume.py:205-249 format): header check, "
-                                        "64-slice pinned chunks read from the file (page cache hot, 8 preadv threads) "
-                                        "overlapped with H2D + fused pass, atlases back to host (session reused)",
-                            "ms_per_volume": min(ts) * 1e3, "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9,
-                            "host_bytes_held": 3 * 64 * ny * nx + 3 * ny * nx}
-    # atlas PNG writing: the c2 step's 14 atlases (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2)
-    # as save_slicemaps writes them -- device filter + parallel deflate vs Pillow (slicemap.py:164)
-    import io
-    from PIL import Image
-    from paper_2311_15038_b200.png import encode_pngs, encode_pngs_device
-    vol = synth.generate(spec, device=device)
-    schemes = {s: AtlasSpec.of(plan_scheme(s)) for s in (512, 256, 128)}
-    res = run_preview(vol, plan_preview(spec.shape, schemes))
-    del vol
-    host = {s: res.atlases[s].cpu().numpy() for s in schemes}
-    encode_pngs(res.atlases[128])  # warm-up
-    t0 = time.perf_counter()
-    ours = sum(len(b) for b in encode_pngs([res.atlases[s] for s in schemes]))
-    t_ours = time.perf_counter() - t0
-    encode_pngs_device(res.atlases[128])  # warm-up
-    t0 = time.perf_counter()
-    dev_bytes = sum(len(b) for b in encode_pngs_device([res.atlases[s] for s in schemes]))
-    t_dev = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    pil = 0
-    for s in schemes:
-        for a in host[s]:
-            buf = io.BytesIO()
-            Image.fromarray(a, mode="L").save(buf, format="PNG")
-            pil += buf.tell()
-    t_pil = time.perf_counter() - t0
-    out["c2_png"] = {"workload": "c2 atlases to PNG bytes (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2): device scanline "
-                                 "filter + parallel zlib-6 deflate blocks vs Pillow single-threaded (slicemap.py:164)",
-                     "ms": t_ours * 1e3, "bytes": ours, "pillow_ms": t_pil * 1e3, "pillow_bytes": pil,
-                     "device_deflate_ms": t_dev * 1e3, "device_deflate_bytes": dev_bytes,
-                     "host_threads": os.cpu_count()}
-    del res
-    torch.cuda.empty_cache()
+        host = {s: res.atlases[s].cpu().numpy() for s in schemes}
+        encode_pngs(res.atlases[128])  # warm-up
+        t0 = time.perf_counter()
+        ours = sum(len(b) for b in encode_pngs([res.atlases[s] for s in schemes]))
+        t_ours = time.perf_counter() - t0
+        encode_pngs_device(res.atlases[128])  # warm-up
+        t0 = time.perf_counter()
+        dev_bytes = sum(len(b) for b in encode_pngs_device([res.atlases[s] for s in schemes]))
+        t_dev = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pil = 0
+        for s in schemes:
+            for a in host[s]:
+                buf = io.BytesIO()
+                Image.fromarray(a, mode="L").save(buf, format="PNG")
+                pil += buf.tell()
+        t_pil = time.perf_counter() - t0
+        out["c2_png"] = {"workload": "c2 atlases to PNG bytes (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2): device scanline "
+                                     "filter + parallel zlib-6 deflate blocks vs Pillow single-threaded (slicemap.py:164)",
+                         "ms": t_ours * 1e3, "bytes": ours, "pillow_ms": t_pil * 1e3, "pillow_bytes": pil,
+                         "device_deflate_ms": t_dev * 1e3, "device_deflate_bytes": dev_bytes,
+                         "host_threads": os.cpu_count()}
+        del res
+        torch.cuda.empty_cache()
+
+
+    for name, fn in (("c1", _c1), ("c3", _c3), ("c4_alpha", _c4_alpha), ("c5", _c5), ("c2_ingest", _c2_ingest),
+                     ("c2_png", _c2_png)):
+        try:  # one side measurement failing (e.g. memory) must not cost the bench line
+            fn()
+        except Exception as e:  # pragma: no cover - reported in the JSON line
+            out[name] = {"error": repr(e)[:300]}
+        torch.cuda.empty_cache()
     return out
 
 
