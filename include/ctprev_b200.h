@@ -231,12 +231,13 @@ int ctp_image_hist_u8(const uint8_t* imgs, int32_t n_images, int64_t pixels,
 
 /* PNG scanline filtering for save_slicemaps (slicemap.py:158-166, which
  * writes every atlas with Pillow): for each row of n_images grayscale
- * images (height x width, u8) picks the PNG filter (None/Sub/Up/Average/
- * Paeth, bpp 1) with the smallest sum of |signed residual| (ties: lowest
- * type) and writes [filter byte, residuals] -- out is
- * n_images x height x (width + 1) bytes, the raw stream a PNG IDAT deflates. */
+ * images (height x width, u8) applies PNG filter `filter` (0..4: None/Sub/
+ * Up/Average/Paeth, bpp 1) or, with filter = -1, the one whose residual
+ * bytes have the lowest order-0 entropy in the row, and writes [filter byte,
+ * residuals] -- out is n_images x height x (width + 1) bytes, the raw stream
+ * a PNG IDAT deflates. */
 int ctp_png_filter_u8(const uint8_t* images, int32_t n_images, int64_t height, int64_t width,
-                      uint8_t* out, void* stream);
+                      int32_t filter, uint8_t* out, void* stream);
 
 /* DEFLATE (RFC 1951) of n_streams byte streams of stream_len bytes each (the
  * PNG-filtered scanlines of ctp_png_filter_u8): every stream is cut into

