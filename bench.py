@@ -603,7 +603,15 @@ def bench_other_configs(device):
         ms = _time_steps(lambda: dev.render(vol, views, channels=4, fp32=True, out=img), 2, warmup=1)
         out["c4_alpha"] = {"workload": "36 azimuths x 1024^2 RGBA8, front-to-back alpha, 4-point TF, early stop 0.99, "
                                        f"{steps} steps", "frames_per_s": 36 / (ms * 1e-3), "ms_per_frame": ms / 36}
-        del vol, img
+        # the reference's own additive mode, fp64 and bit-identical to render.py (5.03 s/view on
+        # the host, 8 numba threads)
+        views = [ViewParams(azimuth_deg=10.0 * k, image_dim=1024, steps=steps, mode="additive") for k in range(8)]
+        g = dev.render(vol, views, channels=1, fp32=False)
+        ms = _time_steps(lambda: dev.render(vol, views, channels=1, fp32=False, out=g), 1, warmup=1)
+        out["c4_additive_exact"] = {"workload": f"8 azimuths x 1024^2, additive (render.py:125-146), {steps} steps, fp64 "
+                                                "bit-identical to the reference", "frames_per_s": 8 / (ms * 1e-3),
+                                    "ms_per_frame": ms / 8, "reference_s_per_frame": 5.03}
+        del vol, img, g
         torch.cuda.empty_cache()
 
     def _c5():
