@@ -45,8 +45,12 @@ constexpr uint32_t kCountCap = (1u << 20) - 1;  // 20-bit count field
 constexpr int kBoxX = 256;                      // TMA box limit per dimension (elements)
 
 template <typename T> struct Vox;
+// u8: [bin][lane] counter words in 256-byte bin rows (lanes in words 0..31,
+// words 32..63 unused) so that a voxel's table offset (v << 8) | (lane << 2) is
+// ONE byte permute of the voxel word with the lane byte, and the table base a
+// warp-uniform operand of the atomic ([R+UR]): PRMT + ATOMS per voxel.
 template <> struct Vox<uint8_t> {
-  static constexpr int UXW = 16, NBINS = 256, HWORDS = 256 * 32;
+  static constexpr int UXW = 16, NBINS = 256, ROWW = 64, HWORDS = 256 * ROWW;
 };
 // u16: COLS interleaved columns [bin][lane % COLS] -- lanes of different columns
 // never share a bank, so the random-bin conflict degree of a warp-wide ATOMS
@@ -126,7 +130,7 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads
       uint32_t s = 0;
 #pragma unroll 8
       for (int k = 0; k < 32; k++) {
-        const int idx = bin * 32 + ((k + bin) & 31);  // rotated: conflict-free
+        const int idx = bin * Vox<uint8_t>::ROWW + ((k + bin) & 31);  // rotated: conflict-free
         const uint32_t wv = hs[idx];
         s += wv >> 12;
         hs[idx] = wv & 0xFFFu;
@@ -150,16 +154,18 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads
 }
 
 // One 16-byte row vector of a unit: UXW atomics; returns the old counter words.
+// u8: tbl = table base (uniform), lb = 4 * lane; u16: lb = table base + column.
 template <typename T>
-__device__ __forceinline__ void row_atomics(const uint4& q, uint32_t lb, uint32_t* o) {
+__device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32_t lb, uint32_t* o) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
   if constexpr (sizeof(T) == 1) {
 #pragma unroll
     for (int k = 0; k < 4; k++)
 #pragma unroll
       for (int b = 0; b < 4; b++) {
-        const uint32_t v = __byte_perm(w[k], 0u, 0x4440u | (uint32_t)b);
-        o[4 * k + b] = atom_add_shared(lb + (v << 7), kOne);  // [bin][lane] words: bin row = 128 B
+        // [0, 0, v, 4*lane] = (v << 8) | (lane << 2): the voxel's counter word
+        const uint32_t off = __byte_perm(w[k], lb, 0x7604u | ((uint32_t)b << 4));
+        o[4 * k + b] = atom_add_shared(tbl + off, kOne);
       }
   } else {
     constexpr uint32_t SH = 2 + (Vox<uint16_t>::COLS == 1 ? 0 : Vox<uint16_t>::COLS == 2 ? 1 : Vox<uint16_t>::COLS == 4 ? 2 : 3);
@@ -303,11 +309,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   // counter words: LUT value in the low byte, count 0
   for (int i = threadIdx.x; i < HW; i += THREADS) {
-    const int bin = (sizeof(T) == 2) ? i / Vox<uint16_t>::COLS : (i >> 5);
+    const int bin = (sizeof(T) == 2) ? i / Vox<uint16_t>::COLS : (i >> 6);
     hs[i] = a.top ? (uint32_t)slut[bin] : (a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255));
   }
   const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
-  const uint32_t lb = (sizeof(T) == 2) ? tbl + 4u * (uint32_t)(lane % Vox<uint16_t>::COLS) : tbl + 4u * (uint32_t)lane;
+  const uint32_t lb = (sizeof(T) == 2) ? tbl + 4u * (uint32_t)(lane % Vox<uint16_t>::COLS) : 4u * (uint32_t)lane;
 
   // unit slots of this thread (same in every tile): coordinates + stage offset
   int uxu[UPT], uyr[UPT], uzr[UPT];
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int h = 0; h < (L >= 1 ? 2 : 1); h++) {
           const int rr = r2 + h;
           const uint4 q = lds128(sbase + uso[i] + (rr / UZ) * row_dz + (rr % UZ) * row_dy);
-          row_atomics<T>(q, lb, o[h]);
+          row_atomics<T>(q, tbl, lb, o[h]);
           if (want0) {  // level 0: the filtered voxels themselves
             uint8_t* dst = a.lv[0].out + level_offset<POW2>(a.lv[0], z + rr / UZ, y + rr % UZ, x);
             uint32_t pk[UXW / 4];
@@ -603,7 +609,7 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
 template <typename T, int L, int THREADS, int NST, int MAXU, bool WANT0, bool POW2>
 static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
   constexpr size_t sm = smem_bytes<T, L, NST, MAXU, THREADS>();
-  if constexpr (sm > 227 * 1024 - 4096) {  // a variant that does not fit this table layout
+  if constexpr (sm > 227 * 1024 - 1024) {  // a variant that does not fit (static smem: < 1 KB)
     set_error("preview: launch shape needs %zu bytes of shared memory", sm);
     return CTP_E_UNSUPPORTED;
   } else {

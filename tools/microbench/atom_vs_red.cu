@@ -5,6 +5,9 @@
 //   B: red.shared.add (no return) on [bin][lane] counters + ld.shared of the LUT
 //      from a separate [bin][lane] word table
 //   C: red.shared.add only (histogram without the LUT: the lower bound)
+//   D: A with [bin][64-word] rows (256 B per bin, lanes in words 0..31): the
+//      address offset (v << 8) | (lane << 2) is ONE PRMT merging the voxel byte
+//      with the lane byte, the table base is a uniform register ([R+UR])
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o atom_vs_red atom_vs_red.cu
 #include <cstdio>
 #include <cstdint>
@@ -13,7 +16,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 
 constexpr int kStage = 65536;
-constexpr int kReps = 64;
+constexpr int kReps = 1024;
 
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
@@ -23,8 +26,8 @@ template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k(unsigned long long* sink) {
   extern __shared__ __align__(16) uint32_t sm[];
   uint4* st = reinterpret_cast<uint4*>(sm);
-  uint32_t* cnt = sm + kStage / 4;         // 256 x 32 words
-  uint32_t* lut = cnt + 256 * 32;          // 256 x 32 words
+  uint32_t* cnt = sm + kStage / 4;         // 256 x 32 words (D: 256 x 64)
+  uint32_t* lut = cnt + 256 * 64;          // 256 x 32 words
   for (int i = threadIdx.x; i < kStage / 4; i += 1024) {
     const uint32_t h = mix32(i * 2654435761u + blockIdx.x);
     uint32_t w = 0;
@@ -37,12 +40,15 @@ __global__ void __launch_bounds__(1024, 1) k(unsigned long long* sink) {
     }
     sm[i] = w;
   }
-  for (int i = threadIdx.x; i < 256 * 32; i += 1024) { cnt[i] = (uint32_t)(i >> 5); lut[i] = (uint32_t)(i >> 5); }
+  for (int i = threadIdx.x; i < 256 * 64; i += 1024) cnt[i] = (uint32_t)(i >> (MODE == 3 ? 6 : 5));
+  for (int i = threadIdx.x; i < 256 * 32; i += 1024) lut[i] = (uint32_t)(i >> 5);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint32_t cb = (uint32_t)__cvta_generic_to_shared(cnt) + 4u * lane;
   const uint32_t lb = (uint32_t)__cvta_generic_to_shared(lut) + 4u * lane;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(st);
+  const uint32_t cb0 = (uint32_t)__cvta_generic_to_shared(cnt);
+  const uint32_t lane4 = 4u * lane;
   uint32_t acc = 0;
   for (int r = 0; r < kReps; r++) {
     for (int i = threadIdx.x; i < kStage / 16; i += 1024) {
@@ -54,7 +60,12 @@ __global__ void __launch_bounds__(1024, 1) k(unsigned long long* sink) {
 #pragma unroll
         for (int b = 0; b < 4; b++) {
           const uint32_t v = __byte_perm(w[kk], 0u, 0x4440u | (uint32_t)b);
-          if (MODE == 0) {
+          if (MODE == 3) {
+            uint32_t old;
+            const uint32_t off = __byte_perm(w[kk], lane4, 0x7604u | ((uint32_t)b << 4));  // [b3 b2 v 4*lane]
+            asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(cb0 + off), "r"(4096u));
+            acc += old;
+          } else if (MODE == 0) {
             uint32_t old;
             asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(cb + (v << 7)), "r"(4096u));
             acc += old;
@@ -74,7 +85,7 @@ __global__ void __launch_bounds__(1024, 1) k(unsigned long long* sink) {
 
 template <int MODE>
 int run(int sms, unsigned long long* sink, const char* name) {
-  const int smem = kStage + 2 * 256 * 32 * 4;
+  const int smem = kStage + 3 * 256 * 32 * 4;
   CK(cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k<MODE><<<sms, 1024, smem>>>(sink);
   CK(cudaDeviceSynchronize());
@@ -100,7 +111,8 @@ int main() {
   CK(cudaMalloc(&sink, 8));
   printf("u8 histogram + LUT, data in shared memory, 1024 thr x %d CTAs\n", sms);
   if (run<0>(sms, sink, "A atom-with-return (LUT in word)") || run<1>(sms, sink, "B red + ld LUT") ||
-      run<2>(sms, sink, "C red only (no LUT)"))
+      run<2>(sms, sink, "C red only (no LUT)") || run<3>(sms, sink, "D atom, one-PRMT address") ||
+      run<0>(sms, sink, "A atom-with-return (LUT in word)") || run<3>(sms, sink, "D atom, one-PRMT address"))
     return 1;
   return 0;
 }
