@@ -685,6 +685,9 @@ static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
     case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
     case 3: return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
     case 4: return launch_v<T, L, 512, 2, 512>(a, vol, st);
+    case 5: return launch_v<T, L, 1024, 4, 512>(a, vol, st);
+    case 6: return launch_v<T, L, 1024, 3, 512>(a, vol, st);
+    case 7: return launch_v<T, L, 512, 4, 512>(a, vol, st);
     default:
       if constexpr (sizeof(T) == 1) {
         // small volumes (config 1: 16 MiB) are latency-bound: 16 warps/SM finish the
