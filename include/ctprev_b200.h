@@ -109,6 +109,13 @@ int ctp_artifact_lut(const void* vol, int32_t elem_bytes, int64_t nz, int64_t ny
 int ctp_lut_apply_u8(const uint8_t* in, uint8_t* out, int64_t n, const uint8_t* lut,
                      uint64_t* hist, void* stream);
 
+/* Extension (uint16, 12-bit; the any-size companion of ctp_preview_u16 for rows
+ * that are not whole 16-byte vectors): out[i] = lut4096[min(in[i], 4095)] over
+ * n elements (the filter o 16->8 rescale LUT of ctp_lut_build(vmax = 4095)).
+ * If hist4096 != NULL the raw 4096-bin histogram is accumulated in the same pass. */
+int ctp_lut_apply_u16(const uint16_t* in, uint8_t* out, int64_t n, const uint8_t* lut4096,
+                      uint64_t* hist4096, void* stream);
+
 /* ---------------- fused preview pass (kernels 1+2+3+4) ------------------ */
 
 /* One HBM pass over a (z-slab of a) uint8 volume:

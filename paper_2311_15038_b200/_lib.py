@@ -79,6 +79,7 @@ SIGNATURES = {
     "ctp_hist_u16": [_P, _I64, _I64, _I64, _I64, _I64, _I32, _P, _P],
     "ctp_lut_build": [_P, _I32, C.c_uint64, _I32, _P, _P, _P],
     "ctp_lut_apply_u8": [_P, _P, _I64, _P, _P, _P],
+    "ctp_lut_apply_u16": [_P, _P, _I64, _P, _P, _P],
     "ctp_artifact_lut": [_P, _I32, _I64, _I64, _I64, _I32, C.c_uint64, _I32, _P, _P, _P, _P, _P],
     "ctp_preview_u8": [_P, _I64, _I64, _I64, _I64, _P, _I32, C.POINTER(LevelOut), _P, _P],
     "ctp_preview_u16": [_P, _I64, _I64, _I64, _I64, _P, _I32, C.POINTER(LevelOut), _P, _P],

@@ -5,6 +5,7 @@
 //   ctp_hist_u16      <- extension (4096-bin, 12-bit data)
 //   ctp_lut_build     <- mask.py:215-231 artifact_bins (cutoff test) + mask.py:241-245 (LUT)
 //   ctp_lut_apply_u8  <- mask.py:246 lut[volume.voxels]  (+ optional raw histogram)
+//   ctp_lut_apply_u16 <- extension: filter o 16->8 rescale for any row length (+ 4096-bin histogram)
 //
 // Privatisation (measured in tools/microbench/hist_bench.cu on B200): per-lane
 // columns [bin][lane] of u32 in shared memory, shared by the block's warps.
@@ -190,6 +191,31 @@ __global__ void lut_apply_tail_kernel(const uint8_t* __restrict__ in, uint8_t* _
 }
 
 
+// u16 (12-bit) filter o rescale for any length / alignment (the extension of
+// mask.py:246 the fused pass uses, for rows that are not whole 16-byte
+// vectors): out[i] = lut4096[min(in[i], 4095)], raw 4096-bin histogram in the
+// same pass.  Per-block table of 4096 (lut | count << 12) words: the atomic's
+// old word carries the LUT byte, as in the fused kernel; 20-bit count fields
+// are flushed by the host keeping a block's share below 2^20 elements.
+__global__ void __launch_bounds__(kHistThreads) lut_apply_u16_kernel(const uint16_t* __restrict__ in,
+                                                                     uint8_t* __restrict__ out, int64_t n,
+                                                                     const uint8_t* __restrict__ lut,
+                                                                     unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t hs[4096];
+  for (int i = threadIdx.x; i < 4096; i += kHistThreads) hs[i] = lut[i];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * kHistThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHistThreads) {
+    const uint32_t v = min((uint32_t)__ldcs(in + i), 4095u);
+    out[i] = (uint8_t)atomicAdd(&hs[v], kCountOne);
+  }
+  __syncthreads();
+  if (hist)
+    for (int b = threadIdx.x; b < 4096; b += kHistThreads) {
+      const uint32_t c = hs[b] >> 12;
+      if (c) atomicAdd(hist + b, (unsigned long long)c);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One launch for the whole artifact-LUT step (mask.py:215-231 + 241-245):
 // every CTA histograms a share of the top slab in shared memory and adds it to
@@ -342,6 +368,19 @@ int ctp_artifact_lut(const void* vol, int32_t elem_bytes, int64_t nz, int64_t ny
         static_cast<const uint16_t*>(vol) + (nz - n_top) * slice, n, nbins, (unsigned long long)cutoff_floor,
         rescale_vmax, lut, flags, h, w);
   CTP_CUDA_CHECK_LAUNCH("artifact_lut_kernel");
+  return CTP_OK;
+}
+
+int ctp_lut_apply_u16(const uint16_t* in, uint8_t* out, int64_t n, const uint8_t* lut4096, uint64_t* hist4096,
+                      void* stream) {
+  CTP_REQUIRE(in && out && lut4096, CTP_E_INVALID, "ctp_lut_apply_u16: null pointer");
+  CTP_REQUIRE(n >= 0, CTP_E_INVALID, "negative length");
+  if (n == 0) return CTP_OK;
+  int grid = grid_for(n, kHistThreads, 8);
+  while ((n + (int64_t)grid - 1) / grid >= (1LL << 20) - 1) grid *= 2;  // a block's share fits the count field
+  lut_apply_u16_kernel<<<grid, kHistThreads, 0, as_stream(stream)>>>(in, out, n, lut4096,
+                                                                      reinterpret_cast<unsigned long long*>(hist4096));
+  CTP_CUDA_CHECK_LAUNCH("lut_apply_u16_kernel");
   return CTP_OK;
 }
 

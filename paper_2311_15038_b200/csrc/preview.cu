@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int UXW = LY::UXW, UZ = LY::UZ, ROWS = LY::ROWS, L1PU = LY::L1PU;
   constexpr int TZ = 1 << L;
   constexpr int UPT = MAXU / THREADS;  // unit slots per thread
+  static_assert(MAXU % THREADS == 0 && UPT >= 1, "a tile is a whole number of unit slots per thread");
   constexpr int HW = Vox<T>::HWORDS;
 
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -685,9 +686,7 @@ static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
     case 2: return launch_v<T, L, 512, 3, 512>(a, vol, st);
     case 3: return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
     case 4: return launch_v<T, L, 512, 2, 512>(a, vol, st);
-    case 5: return launch_v<T, L, 1024, 4, 512>(a, vol, st);
-    case 6: return launch_v<T, L, 1024, 3, 512>(a, vol, st);
-    case 7: return launch_v<T, L, 512, 4, 512>(a, vol, st);
+    case 5: return launch_v<T, L, 512, 4, 512>(a, vol, st);
     default:
       if constexpr (sizeof(T) == 1) {
         // small volumes (config 1: 16 MiB) are latency-bound: 16 warps/SM finish the

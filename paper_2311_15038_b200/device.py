@@ -137,6 +137,20 @@ def lut_apply_u8(src: torch.Tensor, lut: torch.Tensor | None, out: torch.Tensor 
     return out
 
 
+def lut_apply_u16(src: torch.Tensor, lut: torch.Tensor, out: torch.Tensor | None = None,
+                  hist: torch.Tensor | None = None) -> torch.Tensor:
+    """Extension: uint16 (12-bit) -> uint8 through the 4096-entry filter o rescale LUT
+    (any shape, any row length); optionally accumulates the raw 4096-bin histogram."""
+    _check_dev(src, torch.uint16, "lut_apply_u16", ndim=None)
+    _check_dev(lut, torch.uint8, "lut_apply_u16 lut", ndim=1)
+    if lut.numel() != NBINS_U16:
+        raise ValueError("lut_apply_u16: the LUT must have 4096 entries")
+    if out is None:
+        out = torch.empty(src.shape, dtype=torch.uint8, device=src.device)
+    _lib.call("ctp_lut_apply_u16", _ptr(src), _ptr(out), src.numel(), _ptr(lut), _ptr(hist), _stream())
+    return out
+
+
 # ---------------------------------------------------------------------------
 # fused pass
 

@@ -96,10 +96,11 @@ def run_preview(vol: torch.Tensor, plan: PreviewPlan, n_top: int = 3, frac: floa
     if hist is None:
         hist = torch.empty(nbins, dtype=torch.int64, device=vol.device)
     nz, ny, nx = vol.shape
-    if vol.dtype == torch.uint8 and nx % 16 and set(plan.fused) == {0}:
-        # rows not 16-byte vectorisable: filter + histogram with the any-size LUT kernel
+    if nx % (16 // vol.element_size()) and set(plan.fused) == {0}:
+        # rows not 16-byte vectorisable: filter (+ rescale) + histogram with the any-size LUT kernels
         lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
-        outs = {0: dev.lut_apply_u8(vol, lut, hist=hist)}
+        apply = dev.lut_apply_u8 if vol.dtype == torch.uint8 else dev.lut_apply_u16
+        outs = {0: apply(vol, lut, hist=hist)}
     else:
         # the whole step (artifact LUT + fused pass) in one cooperative launch
         outs, hist, lut, flags = dev.preview_step(vol, plan.fused, n_top, frac, hist=hist)

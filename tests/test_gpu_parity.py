@@ -105,6 +105,26 @@ def test_hist_u16_device(P, cuda):
     assert np.array_equal(h, O.histogram_u16(v))
 
 
+def test_lut_apply_u16_any_length(P, cuda):
+    """ctp_lut_apply_u16: filter o rescale + 4096-bin histogram for any element count
+    and offset (incl. values above 4095, which saturate into the last bin)."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(41)
+    bins = frozenset({0, 17, 400, 401, 4095})
+    lut = O.lut_u16(bins)
+    for n in (1, 7, 8, 9, 1000, 65537):
+        v = rng.integers(0, 70000, size=n + 3).astype(np.uint16)[3:]      # odd start offset on the device too
+        src = torch.from_numpy(np.ascontiguousarray(v)).to(cuda)
+        hist = torch.zeros(4096, dtype=torch.int64, device=cuda)
+        out = dev.lut_apply_u16(src, torch.from_numpy(lut).to(cuda), hist=hist).cpu().numpy()
+        assert np.array_equal(out, lut[np.minimum(v, 4095)]), n
+        assert np.array_equal(hist.cpu().numpy(), O.histogram_u16(v)), n
+    full = torch.from_numpy(rng.integers(0, 4096, size=1001).astype(np.uint16)).to(cuda)
+    odd = full[1:]                                                         # a 2-byte-aligned view
+    out = dev.lut_apply_u16(odd, torch.from_numpy(lut).to(cuda)).cpu().numpy()
+    assert np.array_equal(out, lut[odd.cpu().numpy()])
+
+
 def test_filter_unaligned_lengths(P):
     rng = np.random.default_rng(4)
     for shape in [(1, 1, 17), (3, 7, 11), (5, 64, 65)]:
@@ -218,6 +238,53 @@ def test_preview_c2_full_size(P):
     from paper_2311_15038_b200 import synth
     vox = _synth_host(synth.config("c2"))
     _check_preview(P, vox, [512, 256, 128])
+
+
+def _random_volume(rng, dtype, shape):
+    """Seeded data of one of several shapes of histogram: narrow normal, uniform,
+    few distinct values, mostly zero, saturated (u16: incl. values above 4095)."""
+    n = int(np.prod(shape))
+    kind = int(rng.integers(0, 5))
+    top = 255 if dtype == np.uint8 else 4095
+    if kind == 0:
+        v = rng.normal(top * 0.1, top * 0.03, n)
+    elif kind == 1:
+        v = rng.integers(0, top + 1, n)
+    elif kind == 2:
+        v = rng.choice(rng.integers(0, top + 1, 5), n)
+    elif kind == 3:
+        v = np.where(rng.random(n) < 0.9, 0, rng.integers(1, top + 1, n))
+    else:
+        v = np.where(rng.random(n) < 0.5, top, rng.integers(0, top + 1, n))
+        if dtype == np.uint16:
+            v = np.where(rng.random(n) < 0.05, rng.integers(4096, 65536, n), v)
+    hi = 255 if dtype == np.uint8 else 65535
+    return np.clip(np.rint(v), 0, hi).astype(dtype).reshape(shape), kind
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_preview_random_sweep(P, case):
+    """Seeded sweep of the fused pass against the oracle: u8 / u16, shapes with and
+    without 16-byte rows and power-of-two dims (fused vs general path), planned and
+    custom schemes incl. non-power-of-two grids (division addressing) and partial
+    last maps, and five shapes of histogram (artifact bins flag different sets)."""
+    rng = np.random.default_rng(1000 + case)
+    dtype = np.uint8 if case % 3 else np.uint16
+    dims = [int(rng.choice([16, 24, 32, 48, 64, 80, 96, 128])) for _ in range(3)]
+    if case % 4 == 3:
+        dims[2] += int(rng.integers(1, 8))     # rows not a whole number of vectors
+    shape = tuple(dims)                        # (nz, ny, nx)
+    vox, kind = _random_volume(rng, dtype, shape)
+    big = max(shape)
+    schemes = []
+    for s in sorted({int(x) for x in rng.choice([8, 12, 16, 24, 32, 40, 64, 96, 128], 3)}, reverse=True):
+        if s > big:
+            continue
+        g = int(rng.choice([1, 2, 3, 4, 5, 8]))
+        schemes.append(P.SlicemapScheme(s, g * s, g, -(-s // (g * g))))
+    if not schemes:
+        schemes = [P.SlicemapScheme(8, 32, 4, 1)]
+    _check_preview(P, vox, schemes, keep_filtered=bool(case % 2))
 
 
 def test_preview_repeat_bit_identical(P):
