@@ -378,11 +378,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     tz_i = rest / g.tiles_y;
   }
   int k = 0;
+#ifdef CTP_PHASE_TIMING  // per-phase cycle counts (tools/build_variant.py ... -DCTP_PHASE_TIMING)
+  long long t_data = 0, t_units = 0, t_bar = 0, t_lvl = 0;
+  const long long t_start = clock64();
+#endif
   for (int tile = t_begin; tile < t_end; tile++, k++) {
     const int stage = k % NST;
     const uint32_t sbase = stage0 + (uint32_t)stage * LY::STAGE_BYTES;
     const int x0 = tx_i * xw, y0 = ty_i * g.ty, z0 = tz_i * TZ;
+#ifdef CTP_PHASE_TIMING
+    const long long ph0 = clock64();
+#endif
     mbar_wait(bar0 + 8u * stage, (uint32_t)((k / NST) & 1));
+#ifdef CTP_PHASE_TIMING
+    const long long ph1 = clock64();
+#endif
     uint16_t* s1k = s1 + (k & 1) * (LY::S1_BYTES / 2);
     const uint32_t s1off = (uint32_t)(k & 1) * LY::S1_BYTES;
 
@@ -455,7 +465,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     // every thread is done with this stage (and s1 is complete): refill it
+#ifdef CTP_PHASE_TIMING
+    const long long ph2 = clock64();
+#endif
     __syncthreads();
+#ifdef CTP_PHASE_TIMING
+    const long long ph3 = clock64();
+#endif
     if (threadIdx.x == 0 && tile + NST < t_end) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
       issue(tile + NST, stage);
@@ -524,6 +540,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
 
+#ifdef CTP_PHASE_TIMING
+    const long long ph4 = clock64();
+    t_data += ph1 - ph0; t_units += ph2 - ph1; t_bar += ph3 - ph2; t_lvl += ph4 - ph3;
+#endif
     if (++since_flush == g.flush_tiles) {
       since_flush = 0;
       flush_counts<T>(hs, a.hist, THREADS);
@@ -535,6 +555,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   flush_counts<T>(hs, a.hist, THREADS);
+#ifdef CTP_PHASE_TIMING
+  if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) % 8 == 0)
+    printf("PHASE cta %d warp %2d tiles %d total %lld  data-wait %lld  units %lld  barrier %lld  levels+refill %lld\n",
+           (int)blockIdx.x, (int)(threadIdx.x >> 5), k, clock64() - t_start, t_data, t_units, t_bar, t_lvl);
+#endif
 }
 
 template <typename T, int L, int NST, int MAXU, int THREADS>
