@@ -262,7 +262,7 @@ def _random_volume(rng, dtype, shape):
     return np.clip(np.rint(v), 0, hi).astype(dtype).reshape(shape), kind
 
 
-@pytest.mark.parametrize("case", range(12))
+@pytest.mark.parametrize("case", range(18))
 def test_preview_random_sweep(P, case):
     """Seeded sweep of the fused pass against the oracle: u8 / u16, shapes with and
     without 16-byte rows and power-of-two dims (fused vs general path), planned and
@@ -270,20 +270,24 @@ def test_preview_random_sweep(P, case):
     last maps, and five shapes of histogram (artifact bins flag different sets)."""
     rng = np.random.default_rng(1000 + case)
     dtype = np.uint8 if case % 3 else np.uint16
-    dims = [int(rng.choice([16, 24, 32, 48, 64, 80, 96, 128])) for _ in range(3)]
-    if case % 4 == 3:
-        dims[2] += int(rng.integers(1, 8))     # rows not a whole number of vectors
+    if case < 12:
+        dims = [int(rng.choice([16, 24, 32, 48, 64, 80, 96, 128])) for _ in range(3)]
+        if case % 4 == 3:
+            dims[2] += int(rng.integers(1, 8))     # rows not a whole number of vectors
+    else:                                          # tiny and degenerate extents (n_top = 3 <= nz)
+        dims = [int(rng.integers(3, 9)), int(rng.integers(1, 9)), int(rng.choice([1, 5, 8, 16, 17]))]
     shape = tuple(dims)                        # (nz, ny, nx)
     vox, kind = _random_volume(rng, dtype, shape)
     big = max(shape)
     schemes = []
-    for s in sorted({int(x) for x in rng.choice([8, 12, 16, 24, 32, 40, 64, 96, 128], 3)}, reverse=True):
+    sizes = [8, 12, 16, 24, 32, 40, 64, 96, 128] if case < 12 else [1, 2, 3, 4, 6, 8]
+    for s in sorted({int(x) for x in rng.choice(sizes, 3)}, reverse=True):
         if s > big:
             continue
         g = int(rng.choice([1, 2, 3, 4, 5, 8]))
         schemes.append(P.SlicemapScheme(s, g * s, g, -(-s // (g * g))))
     if not schemes:
-        schemes = [P.SlicemapScheme(8, 32, 4, 1)]
+        schemes = [P.SlicemapScheme(1, 2, 2, 1)]
     _check_preview(P, vox, schemes, keep_filtered=bool(case % 2))
 
 
