@@ -44,13 +44,40 @@ struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per
   int64_t vstride;  // bytes between consecutive views' first rows in `out`
 };
 
+// 2x2 footprint of one slice of a layered u8 texture (clamp addressing): the
+// exact voxel values at (x0, y0) .w, (x0+1, y0) .z, (x0, y0+1) .x, (x0+1, y0+1) .y
+__device__ __forceinline__ uint4 tld4_a2d(cudaTextureObject_t tex, int layer, float x, float y) {
+  uint4 r;
+  asm volatile("tld4.r.a2d.v4.u32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(tex), "r"(layer), "f"(x), "f"(y));
+  return r;
+}
+
+// tex != 0: the volume slices [zb, ...) as a layered u8 texture; the eight voxel
+// VALUES then come from two gathers instead of eight byte loads (the texture's
+// clamp addressing is render.py's index clamping), and the arithmetic below is
+// unchanged -- bit-identical results.
 template <typename R>
 __device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R uy, R uz, int nx, int ny, int nz,
-                                        int zb) {
+                                        int zb, cudaTextureObject_t tex = 0) {
   // render.py:68-111
   const R fx0 = floor(ux), fy0 = floor(uy), fz0 = floor(uz);
   int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
   const R fx = ux - (R)x0, fy = uy - (R)y0, fz = uz - (R)z0;
+  if (tex) {
+    const int za = min(max(z0, 0), nz - 1) - zb, zc = min(max(z0 + 1, 0), nz - 1) - zb;
+    const float gxc = (float)x0 + 1.0f, gyc = (float)y0 + 1.0f;
+    const uint4 g0 = tld4_a2d(tex, za, gxc, gyc), g1 = tld4_a2d(tex, zc, gxc, gyc);
+    const R ofx = (R)1 - fx, ofy = (R)1 - fy, ofz = (R)1 - fz;
+    const R c00 = (R)g0.w * ofx + (R)g0.z * fx;
+    const R c10 = (R)g0.x * ofx + (R)g0.y * fx;
+    const R c01 = (R)g1.w * ofx + (R)g1.z * fx;
+    const R c11 = (R)g1.x * ofx + (R)g1.y * fx;
+    const R c0 = c00 * ofy + c10 * fy;
+    const R c1 = c01 * ofy + c11 * fy;
+    return c0 * ofz + c1 * fz;
+  }
   int x1 = x0 + 1, y1 = y0 + 1, z1 = z0 + 1;
   x0 = min(max(x0, 0), nx - 1); y0 = min(max(y0, 0), ny - 1); z0 = min(max(z0, 0), nz - 1);
   x1 = min(max(x1, 0), nx - 1); y1 = min(max(y1, 0), ny - 1); z1 = min(max(z1, 0), nz - 1);
@@ -72,7 +99,7 @@ __device__ __forceinline__ R sample_tri(const uint8_t* __restrict__ vox, R ux, R
 
 template <typename R>
 __device__ __forceinline__ R sample_world(const uint8_t* __restrict__ vox, R px, R py, R pz, R inv_vx, int nx, int ny,
-                                          int nz, int zb) {
+                                          int nz, int zb, cudaTextureObject_t tex = 0) {
   // render.py:114-122
   const R ux = px * inv_vx + (R)(nx - 1) * (R)0.5;
   const R uy = py * inv_vx + (R)(ny - 1) * (R)0.5;
@@ -80,7 +107,7 @@ __device__ __forceinline__ R sample_world(const uint8_t* __restrict__ vox, R px,
   if (ux < (R)-0.5 || ux > (R)nx - (R)0.5 || uy < (R)-0.5 || uy > (R)ny - (R)0.5 || uz < (R)-0.5 ||
       uz > (R)nz - (R)0.5)
     return (R)-1;
-  return sample_tri<R>(vox, ux, uy, uz, nx, ny, nz, zb);
+  return sample_tri<R>(vox, ux, uy, uz, nx, ny, nz, zb, tex);
 }
 
 // Conservative range of k whose sample may lie inside |p_axis| <= half (+ margin).
@@ -125,7 +152,8 @@ __device__ __forceinline__ uint8_t to_u8_unit(R v) {  // floor(min(v, 1) * 255 +
 template <typename R>
 __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__ vox, int zb, int nx, int ny,
                                                      int nz, const __grid_constant__ ViewBatch views, int dim,
-                                                     int row0, int row1, uint8_t* __restrict__ out) {
+                                                     int row0, int row1, uint8_t* __restrict__ out,
+                                                     cudaTextureObject_t tex) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
   const int view = blockIdx.z;
@@ -156,11 +184,27 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
   const R rox = (R)ox, roy = (R)oy, roz = (R)oz;
   const R big_r = (R)G.big_r, dt = (R)G.dt;
 
+  // kUnroll samples are computed independently (their loads in flight together)
+  // and then consumed strictly in k order: every accumulation, comparison and
+  // break happens in the reference's sequence, so results are unchanged.
+  auto sample_at = [&](int k) -> R {
+    const R t = -big_r + ((R)k + (R)0.5) * dt;
+    return sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb, tex);
+  };
+  constexpr int kUnroll = 4;
   if (V.mode == CTP_MODE_ADDITIVE) {  // render.py:125-146
     R acc = 0;
-    for (int k = klo; k <= khi; k++) {
-      const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
+    int k = klo;
+    for (; k + kUnroll - 1 <= khi; k += kUnroll) {
+      R v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) v[u] = sample_at(k + u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+        if (v[u] > (R)0) acc += v[u];
+    }
+    for (; k <= khi; k++) {
+      const R v = sample_at(k);
       if (v > (R)0) acc += v;
     }
     R val = (R)V.gain * acc / (R)steps;
@@ -172,12 +216,12 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     R shade = 0;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb, tex);
       if (v >= thr) {
         R t_lo = t - dt, t_hi = t;
         for (int b = 0; b < 4; b++) {
           const R tm = (R)0.5 * (t_lo + t_hi);
-          const R vm = sample_world<R>(vox, rox + dx * tm, roy + dy * tm, roz, inv_vx, nx, ny, nz, zb);
+          const R vm = sample_world<R>(vox, rox + dx * tm, roy + dy * tm, roz, inv_vx, nx, ny, nz, zb, tex);
           if (vm >= thr) t_hi = tm;
           else t_lo = tm;
         }
@@ -186,9 +230,9 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
         const R ux = hx * inv_vx + (R)(nx - 1) * (R)0.5;
         const R uy = hy * inv_vx + (R)(ny - 1) * (R)0.5;
         const R uz = hz * inv_vx + (R)(nz - 1) * (R)0.5;
-        const R gx = sample_tri<R>(vox, ux + (R)1, uy, uz, nx, ny, nz, zb) - sample_tri<R>(vox, ux - (R)1, uy, uz, nx, ny, nz, zb);
-        const R gy = sample_tri<R>(vox, ux, uy + (R)1, uz, nx, ny, nz, zb) - sample_tri<R>(vox, ux, uy - (R)1, uz, nx, ny, nz, zb);
-        const R gz = sample_tri<R>(vox, ux, uy, uz + (R)1, nx, ny, nz, zb) - sample_tri<R>(vox, ux, uy, uz - (R)1, nx, ny, nz, zb);
+        const R gx = sample_tri<R>(vox, ux + (R)1, uy, uz, nx, ny, nz, zb, tex) - sample_tri<R>(vox, ux - (R)1, uy, uz, nx, ny, nz, zb, tex);
+        const R gy = sample_tri<R>(vox, ux, uy + (R)1, uz, nx, ny, nz, zb, tex) - sample_tri<R>(vox, ux, uy - (R)1, uz, nx, ny, nz, zb, tex);
+        const R gz = sample_tri<R>(vox, ux, uy, uz + (R)1, nx, ny, nz, zb, tex) - sample_tri<R>(vox, ux, uy, uz - (R)1, nx, ny, nz, zb, tex);
         const R gn = sqrt(gx * gx + gy * gy + gz * gz);
         if (gn < (R)1e-12) {
           shade = 1;
@@ -203,9 +247,16 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     for (int c = 0; c < ch; c++) dst[c] = (c == 3) ? 255 : o;
   } else if (V.mode == CTP_MODE_MIP) {
     R m = 0;
-    for (int k = klo; k <= khi; k++) {
-      const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
+    int k = klo;
+    for (; k + kUnroll - 1 <= khi; k += kUnroll) {
+      R v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) v[u] = sample_at(k + u);
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) m = v[u] > m ? v[u] : m;
+    }
+    for (; k <= khi; k++) {
+      const R v = sample_at(k);
       m = v > m ? v : m;
     }
     if (m > (R)255) m = (R)255;
@@ -216,7 +267,7 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
     const R stop = (R)V.early_stop;
     for (int k = klo; k <= khi; k++) {
       const R t = -big_r + ((R)k + (R)0.5) * dt;
-      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb);
+      const R v = sample_world<R>(vox, rox + dx * t, roy + dy * t, roz, inv_vx, nx, ny, nz, zb, tex);
       if (v < (R)0) continue;
       R c[4];
       tf_eval<R>(V.tf, V.slope, v, c);
@@ -246,13 +297,6 @@ __global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__
 // z0 and of slice z1) instead of eight byte loads.  The geometry, sample
 // positions, clamping and skip rule are those of render.py:68-140; the
 // interpolation weights are computed in fp32 (tolerance 1/255).
-__device__ __forceinline__ uint4 tld4_a2d(cudaTextureObject_t tex, int layer, float x, float y) {
-  uint4 r;
-  asm volatile("tld4.r.a2d.v4.u32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(tex), "r"(layer), "f"(x), "f"(y));
-  return r;
-}
 
 template <int MODE>
 __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex, int zb, int nx, int ny, int nz,
@@ -787,10 +831,35 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
     CTP_CUDA_CALL(cudaStreamSynchronize(st));
     return CTP_OK;
   }
+  // fp64 (the reference's modes, bit-exact): the voxel values through two texture
+  // gathers per sample instead of eight scattered byte loads, which saturated L1
+  // (ncu: L1/TEX 99%, issue 12%); the arithmetic is unchanged.  The texture is a
+  // copy of the slab made per call, so it is used where every ray walks its whole
+  // window (additive / MIP / alpha) and the walk dwarfs the copy; surface rays stop
+  // at the first hit and keep the byte loads.
+  const double walk = (double)n_views * (double)(row1 - row0) * dim * v0.steps;
+  const char* fe = getenv("CTP_RENDER_FP64_TEX");  // "0": never, "1": always (tests), else the rule above
+  const bool fp64_tex = (fe && fe[0] == '1') ? true
+                        : (fe && fe[0] == '0') ? false
+                                               : (v0.mode != CTP_MODE_SURFACE && walk >= 16.0 * (double)snz * ny * nx);
+  if (!v0.fp32 && fp64_tex && snz <= 2048 && nx <= 32768 && ny <= 32768) {
+    {
+      TexVolume tv;
+      int rc = make_tex_volume(tv, vol, snz, ny, nx, st);
+      if (rc != CTP_OK) return rc;
+      render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                  (int)row1, out, tv.tex);
+      CTP_CUDA_CHECK_LAUNCH("render_kernel");
+      CTP_CUDA_CALL(cudaStreamSynchronize(st));  // the array / texture object must outlive the kernel
+      return CTP_OK;
+    }
+  }
   if (v0.fp32)
-    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
+    render_kernel<float><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1,
+                                               out, 0);
   else
-    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1, out);
+    render_kernel<double><<<grid, 128, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0, (int)row1,
+                                                out, 0);
   CTP_CUDA_CHECK_LAUNCH("render_kernel");
   return CTP_OK;
 }

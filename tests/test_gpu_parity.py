@@ -521,6 +521,28 @@ def test_c4_full_size_mip_rows_vs_exact_path(P, cuda):
     torch.cuda.empty_cache()
 
 
+def test_fp64_texture_gathers_identical_to_byte_loads(P, cuda, monkeypatch):
+    """The fp64 (reference-mode) renderer reads the eight voxels of a sample through
+    two texture gathers (by default for additive / MIP / alpha batches that walk
+    much more than the slab copy; forced here for every mode incl. surface with its
+    bisection and gradient); the images must equal the byte-load path bit for bit,
+    on odd and anisotropic shapes, whole images and row bands."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(91)
+    for shape, dim, steps in [((40, 33, 70), 48, 96), ((17, 90, 50), 64, 100), ((64, 64, 64), 40, 64)]:
+        vol = torch.from_numpy(_shell_volume(shape, seed=int(rng.integers(0, 99)))).to(cuda)
+        for mode in ("surface", "additive", "mip", "alpha"):
+            views = [P.ViewParams(azimuth_deg=float(rng.uniform(0, 360)), image_dim=dim, steps=steps, mode=mode,
+                                  threshold=int(rng.integers(60, 200))) for _ in range(3)]
+            ch = 4 if mode in ("mip", "alpha") else 1
+            for rows in (None, (dim // 4, dim // 4 + 5)):
+                monkeypatch.setenv("CTP_RENDER_FP64_TEX", "1")
+                a = dev.render(vol, views, channels=ch, fp32=False, rows=rows).cpu().numpy()
+                monkeypatch.setenv("CTP_RENDER_FP64_TEX", "0")
+                b = dev.render(vol, views, channels=ch, fp32=False, rows=rows).cpu().numpy()
+                assert np.array_equal(a, b), (shape, mode, rows)
+
+
 # ---------------------------------------------------------------- z-slab (sort-last) rendering, empty-space skipping
 
 def _shell_volume(shape, seed=3):
