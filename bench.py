@@ -27,8 +27,10 @@ ctprev) on the box's host cores, process pool over z-slabs, bounded sample.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -51,10 +53,12 @@ def _peaks():
 
 
 class ClockSampler:
-    """Continuous nvidia-smi sampling (every 50 ms); samples are tagged with the
-    host clock so only those taken inside the timed region are summarised."""
+    """Continuous nvidia-smi sampling (every 50 ms).  Each sample carries
+    nvidia-smi's own timestamp (its stdout reaches us in bursts when piped, so
+    the arrival time is not the sampling time), and only samples taken inside
+    the timed region (wall clock) are summarised."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -66,9 +70,11 @@ class ClockSampler:
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            cmd = ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                   "-lms", "50"]
+            if shutil.which("stdbuf"):
+                cmd = ["stdbuf", "-oL"] + cmd
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             threading.Thread(target=self._read, daemon=True).start()
             time.sleep(0.3)
         except Exception:
@@ -78,17 +84,21 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.strip().split(",")]
-            if len(parts) >= 7:
-                self.rows.append((time.perf_counter(), parts))
+            if len(parts) >= 8:
+                try:  # "YYYY/MM/DD HH:MM:SS.mmm" (local time)
+                    t = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    t = time.time()
+                self.rows.append((t, parts[1:]))
 
     def mark(self, start: bool):
         if start:
-            self.t0 = time.perf_counter()
+            self.t0 = time.time()
         else:
-            self.t1 = time.perf_counter()
+            self.t1 = time.time()
 
     def __exit__(self, *a):
-        time.sleep(0.12)
+        time.sleep(0.2)
         if self.proc:
             self.proc.terminate()
             try:
