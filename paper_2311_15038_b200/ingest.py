@@ -97,11 +97,12 @@ class RawReader:
 
 
 def preview_from_raw(header_path, schemes=(512, 256, 128), n_top: int = 3, frac: float = 0.0005,
-                     chunk_slices: int = 64, session: PreviewSession | None = None):
+                     chunk_slices: int = 64, session: PreviewSession | None = None, threads: int = 8):
     """``preview_pipeline(load_volume(header_path), schemes)`` without materialising
     the volume on the host: returns the same ``PreviewResult`` (histogram,
     artifact bins, per-scheme SlicemapSets).  Pass a ``session`` to reuse its
-    pinned and device buffers across volumes of one shape."""
+    pinned and device buffers across volumes of one shape; ``threads`` concurrent
+    preadv calls fill each pinned chunk."""
     from .ops import PreviewResult
     shape, raw_path, _ = read_header(header_path)
     sch = {}
@@ -113,7 +114,7 @@ def preview_from_raw(header_path, schemes=(512, 256, 128), n_top: int = 3, frac:
                                  frac=frac, chunk_slices=chunk_slices)
     elif session.shape != shape:
         raise DimensionMismatch(f"session shape {session.shape} != volume {shape}")
-    with RawReader(raw_path, shape) as rd:
+    with RawReader(raw_path, shape, threads=threads) as rd:
         out = session.run_reader(rd)
     slicemaps = {}
     for s, sc in sch.items():
