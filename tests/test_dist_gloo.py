@@ -95,11 +95,14 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(180)
-def test_sharded_preview_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_preview_gloo(world):
+    """z-slab sharding (LUT broadcast from the top-slab owner, histogram all-reduce,
+    atlas cell-row gather to rank 0) equals the whole-volume oracle bit for bit."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
