@@ -28,12 +28,19 @@ dev.preview(v16, lut16, {1: "xyz", 4: AtlasSpec(8, 32, 4, 1)}, hist=h16)
 # stand-alone kernels
 dev.hist_u8(v8, (3, 40))
 dev.lut_apply_u8(v8[:, :, :37].contiguous(), lut, hist=hist)
+dev.lut_apply_u16(v16[:, :, :37].contiguous(), lut16, hist=h16)      # any-length u16 filter o rescale
 dev.downscale(v8, (37, 29, 23))
 dev.encode_atlas(v8[:48, :48, :48].contiguous(), AtlasSpec(64, 512, 8, 1))
 dev.decode_atlas(dev.encode_atlas(v8[:64, :64, :64].contiguous(), AtlasSpec(64, 512, 8, 1)), AtlasSpec(64, 512, 8, 1))
 # renders: exact fp64 modes, fp32 MIP (row planes) and alpha (texture)
 for m in ("surface", "additive"):
     dev.render(v8, [P.ViewParams(azimuth_deg=a, image_dim=32, steps=48, mode=m, threshold=60) for a in (0.0, 37.0)])
+import os  # noqa: E402
+os.environ["CTP_RENDER_FP64_TEX"] = "1"  # fp64 through the texture gathers, every mode
+for m in ("surface", "additive", "mip", "alpha"):
+    dev.render(v8, [P.ViewParams(azimuth_deg=a, image_dim=32, steps=48, mode=m, threshold=60) for a in (0.0, 37.0)],
+               channels=4 if m in ("mip", "alpha") else 1)
+del os.environ["CTP_RENDER_FP64_TEX"]
 dev.render(v8, [P.ViewParams(azimuth_deg=15.0, image_dim=32, steps=48, mode="mip")], channels=4, fp32=True)
 dev.render(v8, [P.ViewParams(azimuth_deg=15.0, image_dim=32, steps=48, mode="alpha")], channels=4, fp32=True)
 dev.image_hist(torch.zeros((3, 16, 16), dtype=torch.uint8, device="cuda"))
