@@ -150,7 +150,8 @@ def _cpu_slab(args):
 
 def cpu_reference_pass(vol, z_lo: int, z_hi: int, pool=None):
     """hist + bins (top slab of the FULL volume) + filter + 3 levels + atlas packing of
-    slices [z_lo, z_hi).  Returns voxels processed."""
+    slices [z_lo, z_hi) (z_lo, z_hi multiples of 8: whole level-3 cells; only the
+    atlas maps those slices fall in are packed).  Returns voxels processed."""
     import numpy as np
     from oracle import ctp_oracle as O
     bins = O.artifact_bins(vol)                          # mask.py:215-231 (top 3 slices)
@@ -159,17 +160,23 @@ def cpu_reference_pass(vol, z_lo: int, z_hi: int, pool=None):
     tasks = [(z, min(z + slab, z_hi), lut) for z in range(z_lo, z_hi, slab)]
     results = pool.map(_cpu_slab, tasks) if pool else list(map(_cpu_slab, tasks))
     hist = np.zeros(256, dtype=np.int64)
-    levels = {s: np.zeros((vol.shape[0] * s // vol.shape[2], s, s), dtype=np.uint8) for s in SCHEMES}
+    nx = vol.shape[2]
+    levels = {s: np.zeros(((z_hi - z_lo) * s // nx, s, s), dtype=np.uint8) for s in SCHEMES}
     for z0, h, out in results:
         hist += h
         for s, lv in zip(SCHEMES, out):
-            r = vol.shape[2] // s
-            levels[s][z0 // r: z0 // r + lv.shape[0]] = lv
+            r = nx // s
+            levels[s][(z0 - z_lo) // r: (z0 - z_lo) // r + lv.shape[0]] = lv
     for s in SCHEMES:                                    # slicemap.py:132-141 packing
         sc = O.plan_scheme(s)
         g = sc[2]
-        for m in range(sc[3]):
-            blk = levels[s][m * g * g:(m + 1) * g * g]
+        per = g * g
+        r = nx // s
+        lz0, lz1 = z_lo // r, z_hi // r
+        for m in range(lz0 // per, -(-lz1 // per)):
+            blk = np.zeros((per, s, s), dtype=np.uint8)
+            a0, a1 = max(m * per, lz0), min((m + 1) * per, lz1)
+            blk[a0 - m * per:a1 - m * per] = levels[s][a0 - lz0:a1 - lz0]
             _ = blk.reshape(g, g, s, s).transpose(0, 2, 1, 3).reshape(g * s, g * s).copy()
     return (z_hi - z_lo) * vol.shape[1] * vol.shape[2]
 
@@ -201,9 +208,9 @@ def run_reference(args):
         t = time.perf_counter()
         cpu_reference_pass(_CPU_VOL, 0, 64, pool)
         per_slice = (time.perf_counter() - t) / 64
-        # size each step so the whole run stays around ~2 minutes
+        # size each step so the whole run stays around ~2 minutes (whole level-3 cells: multiples of 8)
         budget_s = 120.0 / max(1, args.steps + args.warmup)
-        sample = int(max(64, min(1024, budget_s / max(per_slice, 1e-6))) // 64 * 64)
+        sample = int(max(8, min(1024, budget_s / max(per_slice, 1e-6))) // 8 * 8)
         for _ in range(args.warmup):
             cpu_reference_pass(_CPU_VOL, 0, sample, pool)
         t0 = time.perf_counter()
