@@ -642,6 +642,51 @@ def bench_other_configs(device):
         out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume: hist + filter o rescale + L1..L4 padded "
                                  "atlases + 36-view 512^2 MIP strip (from L2), one volume per GPU",
                      "ms_per_volume": ms, "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6}
+        # end to end: volumes from pinned host memory (H2D of volume i+1 on a copy stream while volume i is
+        # reduced; two device buffers), every product read back (atlases + thumbnails, D2H), 4 volumes
+        try:
+            host = torch.empty(spec.shape, dtype=torch.uint16, pin_memory=True)
+            host.copy_(vol)
+            bufs = [vol, torch.empty_like(vol)]
+            prod = sum(t.numel() for t in ps.atlases.values()) + ps.thumbs.numel()
+            host_out = torch.empty(prod, dtype=torch.uint8, pin_memory=True)
+            cs = torch.cuda.Stream()
+            main = torch.cuda.current_stream()
+            n_vol = 4
+            done = [torch.cuda.Event() for _ in range(2)]
+            loaded = [torch.cuda.Event() for _ in range(2)]
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            with torch.cuda.stream(cs):
+                bufs[0].copy_(host, non_blocking=True)
+                loaded[0].record(cs)
+            for q in range(n_vol):
+                b = q % 2
+                if q + 1 < n_vol:
+                    with torch.cuda.stream(cs):
+                        if q >= 1:
+                            cs.wait_event(done[1 - b])
+                        bufs[1 - b].copy_(host, non_blocking=True)
+                        loaded[1 - b].record(cs)
+                main.wait_event(loaded[b])
+                r = ps.process(bufs[b])
+                done[b].record(main)
+                o = 0
+                for t in list(r.atlases.values()) + [r.thumbs]:
+                    host_out[o:o + t.numel()].copy_(t.reshape(-1), non_blocking=True)
+                    o += t.numel()
+            e1.record(main)
+            torch.cuda.synchronize()
+            ms_e2e = e0.elapsed_time(e1) / n_vol
+            out["c5"]["e2e"] = {"ms_per_volume": ms_e2e, "volumes_per_min_per_gpu": 60000.0 / ms_e2e,
+                                "h2d_bytes_per_volume": host.numel() * 2, "d2h_bytes_per_volume": prod,
+                                "path": "pinned host volume -> H2D (copy stream, double-buffered) -> PreviewStream."
+                                        "process -> atlases + thumbnails D2H into pinned memory"}
+            del host, host_out, bufs
+        except Exception as e:  # pinned 9 GiB may not be available on every host
+            out["c5"]["e2e"] = {"error": repr(e)[:200]}
         del vol, ps
         torch.cuda.empty_cache()
 
