@@ -599,7 +599,13 @@ static int make_tmap(CUtensorMap* map, const T* vol, const PvGeom& g, int tz) {
   return CTP_OK;
 }
 
-// tile geometry for at most `maxu` units per tile; boxes of <= 256 x-elements
+// tile geometry for at most `maxu` units per tile; boxes of <= 256 x-elements.
+// Rows are staged whole when a 2^L x 2^L block row of the full width fits the
+// tile (one box if the row fits in one, else whole boxes, the last one partly
+// out of bounds and zero-filled): then the tile takes as many block rows as fit,
+// so every level count keeps tiles of ~maxu units (2^L-row tiles of a wide
+// volume would be 16-64x smaller for L <= 2).  Otherwise tiles are 2^L rows of
+// whole boxes.
 template <typename T>
 static void plan_tiles(PvGeom& g, int nlev, int maxu) {
   constexpr int UXW = Vox<T>::UXW;
@@ -608,9 +614,11 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
   const int64_t blk = 1LL << nlev;
   const int64_t xu_total = g.nx / UXW;
   const int64_t urows_per_block = (int64_t)(tz / uz) * (blk / uz);  // unit rows in a 2^L x 2^L block
-  if (xu_total * urows_per_block <= maxu && xu_total * UXW <= kBoxX) {
+  const int64_t box_u = kBoxX / UXW;
+  const int64_t xu_stage = xu_total <= box_u ? xu_total : ((xu_total + box_u - 1) / box_u) * box_u;
+  if (xu_stage * urows_per_block <= maxu) {
     g.txu = (int)xu_total;
-    int64_t ky = maxu / (xu_total * urows_per_block);
+    int64_t ky = maxu / (xu_stage * urows_per_block);
     const int64_t ky_max = (g.ny + blk - 1) / blk;
     if (ky > ky_max) ky = ky_max;
     if (ky * blk > 256) ky = 256 / blk;  // TMA box rows <= 256
@@ -619,8 +627,7 @@ static void plan_tiles(PvGeom& g, int nlev, int maxu) {
   } else {
     int64_t txu = maxu / urows_per_block;
     if (txu > xu_total) txu = xu_total;
-    const int64_t box_u = kBoxX / UXW;  // a tile wider than one box is whole boxes
-    if (txu > box_u) txu = (txu / box_u) * box_u;
+    if (txu > box_u) txu = (txu / box_u) * box_u;  // a tile wider than one box is whole boxes
     g.txu = (int)txu;
     g.ty = (int)blk;
   }
@@ -665,6 +672,9 @@ static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStrea
 template <typename T, int L, int THREADS, int NST, int MAXU>
 static int launch_v(PvArgs a, const T* vol, cudaStream_t st) {
   plan_tiles<T>(a.g, L, MAXU);
+  constexpr int64_t kStage = PvLayout<T, L, MAXU>::STAGE_BYTES;
+  CTP_REQUIRE((int64_t)a.g.box_bytes * a.g.nboxes <= kStage, CTP_E_UNSUPPORTED,
+              "preview: tile of %d boxes x %u bytes exceeds the stage", a.g.nboxes, a.g.box_bytes);
   const int64_t n_tiles = (int64_t)a.g.tiles_x * a.g.tiles_y * (a.g.nz >> L);
   CTP_REQUIRE(n_tiles < (1LL << 31), CTP_E_INVALID, "preview: too many tiles");
   a.g.n_tiles = (int)n_tiles;
