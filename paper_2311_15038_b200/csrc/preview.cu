@@ -479,23 +479,34 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // ---- levels 2..L from the level-1 sums -------------------------------------------
     if constexpr (L == 2) {
-      const int nx2 = xw >> 2, ny2 = g.ty >> 2;
-      const int cells = ny2 * nx2;  // TZ == 4: one level-2 slice per tile
+      // four x-adjacent level-2 cells per thread: their 8 level-1 x-cells are one
+      // aligned 16-byte run of an s1 row (the swizzle moves 32-byte blocks), one
+      // 4-byte store of the level row
+      const int nq = xw >> 4, ny2 = g.ty >> 2;  // quads of level-2 cells per row, rows
       const bool want2 = a.lv[2].out != nullptr;
-      for (int c = threadIdx.x; c < cells; c += THREADS) {
-        const int x2 = c % nx2, y2 = c / nx2;
-        const int gx = (x0 >> 2) + x2, gy = (y0 >> 2) + y2;
+      for (int c = threadIdx.x; c < ny2 * nq; c += THREADS) {
+        const int q = c % nq, y2 = c / nq;
+        const int gx = (x0 >> 2) + 4 * q, gy = (y0 >> 2) + y2;
         if (gx >= (g.nx >> 2) || gy >= (g.ny >> 2)) continue;
-        uint32_t sum = 0;
+        uint32_t sum[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int ez = 0; ez < 2; ez++)
 #pragma unroll
           for (int ey = 0; ey < 2; ey++) {
-            const uint32_t pair = *reinterpret_cast<const uint32_t*>(
-                s1k + (ez * rows_u + 2 * y2 + ey) * s1_row + ((2 * x2) ^ s1_swz(ez, 2 * y2 + ey)));
-            sum += (pair & 0xFFFFu) + (pair >> 16);
+            const uint4 w = lds128(s1a + s1off +
+                                   2u * (uint32_t)((ez * rows_u + 2 * y2 + ey) * s1_row + ((8 * q) ^ s1_swz(ez, 2 * y2 + ey))));
+            sum[0] += (w.x & 0xFFFFu) + (w.x >> 16);
+            sum[1] += (w.y & 0xFFFFu) + (w.y >> 16);
+            sum[2] += (w.z & 0xFFFFu) + (w.z >> 16);
+            sum[3] += (w.w & 0xFFFFu) + (w.w >> 16);
           }
-        if (want2) a.lv[2].out[level_offset<POW2>(a.lv[2], z0 >> 2, gy, gx)] = (uint8_t)((sum + 32) >> 6);
+        if (want2) {
+          uint8_t* dst = a.lv[2].out + level_offset<POW2>(a.lv[2], z0 >> 2, gy, gx);
+          const uint32_t v = ((sum[0] + 32) >> 6) | (((sum[1] + 32) >> 6) << 8) | (((sum[2] + 32) >> 6) << 16) |
+                             (((sum[3] + 32) >> 6) << 24);
+          if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = v;
+          else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(v >> (8 * b));
+        }
       }
     } else if constexpr (L >= 3) {
       uint32_t sa = 0, sb = 0;  // the two level-2 children of this lane
