@@ -333,38 +333,41 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t row_dy = (uint32_t)g.box_x * sizeof(T);
   const uint32_t row_dz = (uint32_t)g.box_x * g.ty * sizeof(T);
 
-  // Level >= 3 reduction slot (tile-invariant): a group of 4 lanes owns one
-  // level-3 cell; lane q = (dz, dy) reduces the two x-adjacent level-2 children
-  // (2z3+dz, 2y3+dy, 2x3 + {0,1}); level 3 = shfl over the 4 lanes; for L = 4
-  // the 8 level-3 children of a level-4 cell are 8 consecutive groups (a warp).
-  int c_x2 = -1, c_y2 = 0, c_z2 = 0;
+  // Level >= 3 reduction slot (tile-invariant): a lane owns one (z2, y2) row run
+  // of four x-adjacent level-2 cells (x-quad q: level-1 x-cells 8q .. 8q+7, one
+  // aligned 16-byte run of an s1 row); the 4 lanes of a group are (dz, dy) of one
+  // level-3 row (z3, y3) and reduce its two level-3 cells (x3 = 2q, 2q+1) by
+  // shuffles; for L = 4 the 4 groups (z3, y3 parity) of one level-4 cell are 16
+  // consecutive lanes.
+  int c_q = -1, c_y2 = 0, c_z2 = 0;
   uint32_t c_s1 = 0;
   if constexpr (L >= 3) {
-    const int nx3 = xw >> 3, ny3 = g.ty >> 3;
-    const int cells3 = (TZ >> 3) * ny3 * nx3;
-    const int grp = threadIdx.x >> 2, q = threadIdx.x & 3;
-    if (grp < cells3) {
-      int x3, y3, z3;
-      if constexpr (L == 3) {
-        x3 = grp % nx3;
-        y3 = grp / nx3;  // TZ == 8: a single level-3 slice per tile
-        z3 = 0;
-      } else {
-        const int nx4 = nx3 >> 1;
-        const int c4 = grp >> 3, ch = grp & 7;
-        const int x4 = c4 % nx4, y4 = c4 / nx4;  // TZ == 16: a single level-4 slice per tile
-        x3 = 2 * x4 + (ch & 1);
-        y3 = 2 * y4 + ((ch >> 1) & 1);
-        z3 = ch >> 2;
+    const int nq = xw >> 4;  // x-quads of level-2 cells per row (= level-4 cells per row for L = 4)
+    const int grp = threadIdx.x >> 2, ql = threadIdx.x & 3;
+    int q = -1, y3 = 0, z3 = 0;
+    if constexpr (L == 3) {
+      if (grp < nq * (g.ty >> 3)) {  // TZ == 8: a single level-3 slice per tile
+        q = grp % nq;
+        y3 = grp / nq;
       }
-      c_z2 = 2 * z3 + (q >> 1);
-      c_y2 = 2 * y3 + (q & 1);
-      c_x2 = 2 * x3;
-      // first level-1 child row (z1 = 2 z2, y1 = 2 y2), x1 = 2 x2 .. 2 x2 + 3 (swizzled, see s1_swz)
-      c_s1 = s1a + 2u * (uint32_t)(((2 * c_z2) * rows_u + 2 * c_y2) * s1_row +
-                                   ((2 * c_x2) ^ s1_swz(2 * c_z2, 2 * c_y2)));
+    } else {
+      const int cell = grp >> 2, sub = grp & 3;  // TZ == 16: a single level-4 slice per tile
+      if (cell < nq * (g.ty >> 4)) {
+        q = cell % nq;
+        z3 = sub >> 1;
+        y3 = 2 * (cell / nq) + (sub & 1);
+      }
+    }
+    if (q >= 0) {
+      c_q = q;
+      c_z2 = 2 * z3 + (ql >> 1);
+      c_y2 = 2 * y3 + (ql & 1);
+      // first level-1 row of the run (z1 = 2 z2, y1 = 2 y2); the swizzle (bit 1 of y1, z1) is
+      // the same for all four rows the lane reads
+      c_s1 = s1a + 2u * (uint32_t)(((2 * c_z2) * rows_u + 2 * c_y2) * s1_row + ((8 * q) ^ s1_swz(2 * c_z2, 2 * c_y2)));
     }
   }
+  const bool lvl_warp = __any_sync(0xFFFFFFFFu, c_q >= 0);  // warp-uniform: this warp has level work
   __syncthreads();
 
   constexpr bool want0 = WANT0;
@@ -509,44 +512,51 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     } else if constexpr (L >= 3) {
-      uint32_t sa = 0, sb = 0;  // the two level-2 children of this lane
-      if (c_x2 >= 0) {
+      if (lvl_warp) {
+        uint32_t l2[4] = {0, 0, 0, 0};  // four x-adjacent level-2 sums of this lane's (z2, y2) row
+        if (c_q >= 0) {
 #pragma unroll
-        for (int ez = 0; ez < 2; ez++)
+          for (int ez = 0; ez < 2; ez++)
 #pragma unroll
-          for (int ey = 0; ey < 2; ey++) {
-            uint32_t h0, h1;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(h0), "=r"(h1)
-                         : "r"(c_s1 + s1off + 2u * (uint32_t)((ez * rows_u + ey) * s1_row)));
-            sa += (h0 & 0xFFFFu) + (h0 >> 16);
-            sb += (h1 & 0xFFFFu) + (h1 >> 16);
+            for (int ey = 0; ey < 2; ey++) {
+              const uint4 w = lds128(c_s1 + s1off + 2u * (uint32_t)((ez * rows_u + ey) * s1_row));
+              l2[0] += (w.x & 0xFFFFu) + (w.x >> 16);
+              l2[1] += (w.y & 0xFFFFu) + (w.y >> 16);
+              l2[2] += (w.z & 0xFFFFu) + (w.z >> 16);
+              l2[3] += (w.w & 0xFFFFu) + (w.w >> 16);
+            }
+          const int gx = (x0 >> 2) + 4 * c_q, gy = (y0 >> 2) + c_y2;
+          if (a.lv[2].out != nullptr && gx < (g.nx >> 2) && gy < (g.ny >> 2)) {
+            uint8_t* dst = a.lv[2].out + level_offset<POW2>(a.lv[2], (z0 >> 2) + c_z2, gy, gx);
+            const uint32_t v = ((l2[0] + 32) >> 6) | (((l2[1] + 32) >> 6) << 8) | (((l2[2] + 32) >> 6) << 16) |
+                               (((l2[3] + 32) >> 6) << 24);
+            if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) *reinterpret_cast<uint32_t*>(dst) = v;
+            else for (int b = 0; b < 4; b++) dst[b] = (uint8_t)(v >> (8 * b));
           }
-        const int gx = (x0 >> 2) + c_x2, gy = (y0 >> 2) + c_y2;
-        if (a.lv[2].out != nullptr && gx < (g.nx >> 2) && gy < (g.ny >> 2)) {
-          uint8_t* dst = a.lv[2].out + level_offset<POW2>(a.lv[2], (z0 >> 2) + c_z2, gy, gx);
-          const uint32_t v = ((sa + 32) >> 6) | (((sb + 32) >> 6) << 8);
-          if ((reinterpret_cast<uintptr_t>(dst) & 1) == 0) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)v;
-          else { dst[0] = (uint8_t)v; dst[1] = (uint8_t)(v >> 8); }
         }
-      }
-      uint32_t s3v = sa + sb;
-      s3v += __shfl_xor_sync(0xFFFFFFFFu, s3v, 1);
-      s3v += __shfl_xor_sync(0xFFFFFFFFu, s3v, 2);
-      if (c_x2 >= 0 && (threadIdx.x & 3) == 0) {
-        const int gx = (x0 >> 3) + (c_x2 >> 1), gy = (y0 >> 3) + (c_y2 >> 1);
-        if (a.lv[3].out != nullptr && gx < (g.nx >> 3) && gy < (g.ny >> 3))
-          a.lv[3].out[level_offset<POW2>(a.lv[3], (z0 >> 3) + (c_z2 >> 1), gy, gx)] = (uint8_t)((s3v + 256) >> 9);
-      }
-      if constexpr (L == 4) {
-        uint32_t s4v = s3v;
-        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 4);
-        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 8);
-        s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 16);
-        if (c_x2 >= 0 && lane == 0) {
-          const int gx = (x0 >> 4) + (c_x2 >> 2), gy = (y0 >> 4) + (c_y2 >> 2);
-          if (a.lv[4].out != nullptr && gx < (g.nx >> 4) && gy < (g.ny >> 4))
-            a.lv[4].out[level_offset<POW2>(a.lv[4], (z0 >> 4), gy, gx)] = (uint8_t)((s4v + 2048) >> 12);
+        uint32_t s3a = l2[0] + l2[1], s3b = l2[2] + l2[3];  // level-3 cells x3 = 2q, 2q + 1 (partial)
+        s3a += __shfl_xor_sync(0xFFFFFFFFu, s3a, 1);
+        s3b += __shfl_xor_sync(0xFFFFFFFFu, s3b, 1);
+        s3a += __shfl_xor_sync(0xFFFFFFFFu, s3a, 2);
+        s3b += __shfl_xor_sync(0xFFFFFFFFu, s3b, 2);
+        if (c_q >= 0 && (lane & 3) == 0) {
+          const int gx = (x0 >> 3) + 2 * c_q, gy = (y0 >> 3) + (c_y2 >> 1);
+          if (a.lv[3].out != nullptr && gx < (g.nx >> 3) && gy < (g.ny >> 3)) {
+            uint8_t* dst = a.lv[3].out + level_offset<POW2>(a.lv[3], (z0 >> 3) + (c_z2 >> 1), gy, gx);
+            const uint32_t v = ((s3a + 256) >> 9) | (((s3b + 256) >> 9) << 8);
+            if ((reinterpret_cast<uintptr_t>(dst) & 1) == 0) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)v;
+            else { dst[0] = (uint8_t)v; dst[1] = (uint8_t)(v >> 8); }
+          }
+        }
+        if constexpr (L == 4) {
+          uint32_t s4v = s3a + s3b;
+          s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 4);
+          s4v += __shfl_xor_sync(0xFFFFFFFFu, s4v, 8);
+          if (c_q >= 0 && (lane & 15) == 0) {
+            const int gx = (x0 >> 4) + c_q, gy = (y0 >> 4) + (c_y2 >> 2);
+            if (a.lv[4].out != nullptr && gx < (g.nx >> 4) && gy < (g.ny >> 4))
+              a.lv[4].out[level_offset<POW2>(a.lv[4], (z0 >> 4), gy, gx)] = (uint8_t)((s4v + 2048) >> 12);
+          }
         }
       }
     }
