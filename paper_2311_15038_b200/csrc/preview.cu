@@ -725,11 +725,10 @@ static int launch_v(PvArgs a, const T* vol, cudaStream_t st) {
 // Launch-shape variants, selectable with CTP_PREVIEW_VARIANT for tuning
 // (tools/prof_preview.py); the default is the fastest measured on B200.
 static int preview_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once, thread-safe initialisation
     const char* e = getenv("CTP_PREVIEW_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return v;
 }
 
