@@ -292,21 +292,26 @@ def test_preview_random_sweep(P, case):
 
 
 @pytest.mark.parametrize("nx", [784, 1008, 1296])
-def test_preview_wide_rows_multibox_tiles(P, cuda, nx):
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_preview_wide_rows_multibox_tiles(P, cuda, nx, dtype):
     """Rows wider than one TMA box (256 bytes) and not a multiple of it: whole-width
     tiles of several boxes, the last one partly outside the volume (zero-filled),
     with 1, 2, 3 and 4 fused dense levels (the tile planner stacks block rows for
     L <= 2); histogram and every level against the oracle."""
     from paper_2311_15038_b200 import device as dev
     rng = np.random.default_rng(nx)
-    vox, _ = _random_volume(rng, np.uint8, (32, 48, nx))
-    lut = O.filter_lut({0, 3, 17, 200})
-    f = O.apply_lut(vox, lut)
+    vox, _ = _random_volume(rng, dtype, (32, 48, nx))
+    if dtype == np.uint8:
+        lut, h_ref = O.filter_lut({0, 3, 17, 200}), O.histogram(vox)
+        f = O.apply_lut(vox, lut)
+    else:
+        lut, h_ref = O.lut_u16(frozenset({0, 5, 400, 4095})), O.histogram_u16(vox)
+        f = lut[np.minimum(vox, 4095)]
     vol = torch.from_numpy(vox).to(cuda)
     for nlev in (1, 2, 3, 4):
-        hist = torch.zeros(256, dtype=torch.int64, device=cuda)
+        hist = torch.zeros(h_ref.size, dtype=torch.int64, device=cuda)
         outs = dev.preview(vol, torch.from_numpy(lut).to(cuda), {l: "xyz" for l in range(1, nlev + 1)}, hist=hist)
-        assert np.array_equal(hist.cpu().numpy(), O.histogram(vox)), nlev
+        assert np.array_equal(hist.cpu().numpy(), h_ref), nlev
         for l in range(1, nlev + 1):
             ref = O.downscale(f, (nx >> l, 48 >> l, 32 >> l))
             assert np.array_equal(outs[l].cpu().numpy(), ref), (nlev, l)
