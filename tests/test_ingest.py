@@ -112,7 +112,8 @@ def test_preview_from_raw_equals_in_memory(tmp_path, cuda, shape, schemes, chunk
 
 
 @pytest.mark.gpu
-def test_preview_session_host_buffers_equal_in_memory(cuda):
+@pytest.mark.parametrize("u16", [False, True])
+def test_preview_session_host_buffers_equal_in_memory(cuda, u16):
     """PreviewSession.run (pinned host volume -> z-chunk H2D / fused pass / atlas D2H on
     three streams, the bench's e2e path) == the one-launch device step, twice in a row
     (buffers reused)."""
@@ -123,13 +124,17 @@ def test_preview_session_host_buffers_equal_in_memory(cuda):
     rng = np.random.default_rng(5)
     shape = (512, 256, 256)
     schemes = {256: AtlasSpec.of(P.plan_scheme(256)), 128: AtlasSpec.of(P.plan_scheme(128))}
-    sess = PreviewSession(shape, torch.uint8, schemes, chunk_slices=64)
+    sess = PreviewSession(shape, torch.uint16 if u16 else torch.uint8, schemes, chunk_slices=64)
     for it in range(2):
-        vol = np.clip(np.rint(rng.normal(30 + 10 * it, 8, shape)), 0, 255).astype(np.uint8)
-        vol[-3:, :64] = 200
+        if u16:  # 12-bit data (the config-3/5 extension), incl. values that saturate
+            vol = np.clip(np.rint(rng.normal(400 + 100 * it, 120, shape)), 0, 4200).astype(np.uint16)
+            vol[-3:, :64] = 2800
+        else:
+            vol = np.clip(np.rint(rng.normal(30 + 10 * it, 8, shape)), 0, 255).astype(np.uint8)
+            vol[-3:, :64] = 200
         host = torch.from_numpy(vol).pin_memory()
         out = sess.run(host)
-        ref = P.preview_pipeline(P.Volume(vol), schemes=(256, 128))
+        ref = P.preview_pipeline(vol, schemes=(256, 128))  # the array form takes uint16 too
         assert np.array_equal(out["hist"].numpy(), ref.histogram)
         assert frozenset(np.nonzero(out["flags"].numpy())[0].tolist()) == ref.bins
         for s in (256, 128):
