@@ -834,14 +834,15 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
   // fp64 (the reference's modes, bit-exact): the voxel values through two texture
   // gathers per sample instead of eight scattered byte loads, which saturated L1
   // (ncu: L1/TEX 99%, issue 12%); the arithmetic is unchanged.  The texture is a
-  // copy of the slab made per call, so it is used where every ray walks its whole
-  // window (additive / MIP / alpha) and the walk dwarfs the copy; surface rays stop
-  // at the first hit and keep the byte loads.
+  // copy of the slab made per call (one read + one write per voxel), so it is used
+  // where every ray walks its whole window (additive / MIP / alpha) and the batch
+  // takes at least ~2 samples per voxel; surface rays stop at the first hit and
+  // keep the byte loads.
   const double walk = (double)n_views * (double)(row1 - row0) * dim * v0.steps;
   const char* fe = getenv("CTP_RENDER_FP64_TEX");  // "0": never, "1": always (tests), else the rule above
   const bool fp64_tex = (fe && fe[0] == '1') ? true
                         : (fe && fe[0] == '0') ? false
-                                               : (v0.mode != CTP_MODE_SURFACE && walk >= 16.0 * (double)snz * ny * nx);
+                                               : (v0.mode != CTP_MODE_SURFACE && walk >= 2.0 * (double)snz * ny * nx);
   if (!v0.fp32 && fp64_tex && snz <= 2048 && nx <= 32768 && ny <= 32768) {
     {
       TexVolume tv;
