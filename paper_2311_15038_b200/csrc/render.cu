@@ -149,8 +149,11 @@ __device__ __forceinline__ uint8_t to_u8_unit(R v) {  // floor(min(v, 1) * 255 +
   return (uint8_t)(int)floor(v * (R)255 + (R)0.5);
 }
 
+#ifndef CTP_RENDER_MINB
+#define CTP_RENDER_MINB 10  // 10 CTAs of 128 per SM (<= 48 registers): the fp64 walk is latency-bound at 64 registers
+#endif
 template <typename R>
-__global__ void __launch_bounds__(128) render_kernel(const uint8_t* __restrict__ vox, int zb, int nx, int ny,
+__global__ void __launch_bounds__(128, CTP_RENDER_MINB) render_kernel(const uint8_t* __restrict__ vox, int zb, int nx, int ny,
                                                      int nz, const __grid_constant__ ViewBatch views, int dim,
                                                      int row0, int row1, uint8_t* __restrict__ out,
                                                      cudaTextureObject_t tex) {
