@@ -752,15 +752,25 @@ static int launch_l(const PvArgs& a, const T* vol, cudaStream_t st) {
     case 3: return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
     case 4: return launch_v<T, L, 512, 2, 512>(a, vol, st);
     case 5: return launch_v<T, L, 512, 4, 512>(a, vol, st);
-    default:
+    case 6:  // L = 0: 4 one-row units per thread, 64 KB tiles
+      if constexpr (L == 0) return launch_v<T, L, 1024, 2, 4096>(a, vol, st);
+      return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
+    default: {
+      const bool small = (int64_t)a.g.nx * a.g.ny * a.g.nz < (int64_t(1) << 26);
+      // L = 0: a unit is ONE 16-byte row vector, so 4 units per thread keep the tile
+      // at 64 KB (1024-unit tiles were 16 KB: c2 with a level-0 atlas 0.513 -> 0.370 ms)
+      if constexpr (L == 0) {
+        if (!small) return launch_v<T, L, 1024, 2, 4096>(a, vol, st);
+      }
       if constexpr (sizeof(T) == 1) {
         // small volumes (config 1: 16 MiB) are latency-bound: 16 warps/SM finish the
         // handful of tiles per CTA sooner (16.4 vs 18.1 us per graph-replayed step)
-        if ((int64_t)a.g.nx * a.g.ny * a.g.nz < (int64_t(1) << 26)) return launch_v<T, L, 512, 2, 1024>(a, vol, st);
+        if (small) return launch_v<T, L, 512, 2, 1024>(a, vol, st);
         return launch_v<T, L, 1024, 2, 1024>(a, vol, st);
       } else {
         return launch_v<T, L, 512, 2, 1024>(a, vol, st);
       }
+    }
   }
 }
 

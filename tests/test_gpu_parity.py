@@ -317,6 +317,27 @@ def test_preview_wide_rows_multibox_tiles(P, cuda, nx, dtype):
             assert np.array_equal(outs[l].cpu().numpy(), ref), (nlev, l)
 
 
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+def test_preview_level0_large_tiles(P, cuda, dtype):
+    """Level 0 only on a volume above the small-volume threshold (2^26 voxels): four
+    one-row units per thread, 64 KB whole-width tiles of several boxes (the last one
+    partly outside the rows); the filtered voxels and the histogram against the oracle."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(64)
+    vox, _ = _random_volume(rng, dtype, (64, 1024, 1040))
+    if dtype == np.uint8:
+        lut, h_ref = O.filter_lut({0, 3, 17, 200}), O.histogram(vox)
+        f = O.apply_lut(vox, lut)
+    else:
+        lut, h_ref = O.lut_u16(frozenset({0, 5, 400, 4095})), O.histogram_u16(vox)
+        f = lut[np.minimum(vox, 4095)]
+    vol = torch.from_numpy(vox).to(cuda)
+    hist = torch.zeros(h_ref.size, dtype=torch.int64, device=cuda)
+    outs = dev.preview(vol, torch.from_numpy(lut).to(cuda), {0: "xyz"}, hist=hist)
+    assert np.array_equal(hist.cpu().numpy(), h_ref)
+    assert np.array_equal(outs[0].cpu().numpy(), f)
+
+
 def test_preview_repeat_bit_identical(P):
     from paper_2311_15038_b200 import synth
     vox = _synth_host(synth.small((128, 128, 128), seed=10))
