@@ -129,7 +129,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU reference: the numpy oracle port of ctprev's algorithm (oracle/ctp_oracle.py),
 # fanned out over z-slabs on all host cores (exact: hist per slab is summed,
-# the filter is per voxel, downscale is slab-separable on 64-slice slabs)
+# the filter is per voxel, downscale is block-separable on blocks of whole level-3 cells)
 
 _CPU_VOL = None
 
@@ -448,7 +448,7 @@ def main():
             c_s = time.perf_counter() - c0
         cpu = {"value": n / c_s / 1e9, "unit": "GVoxel/s", "cores": workers, "kind": "port",
                "sample": "512 of 1024 z-slices of the same c2 volume: hist + artifact bins + filter + 512/256/128 "
-                         "levels + atlas packing (numpy oracle port of ctprev, process pool over 64-slice slabs)",
+                         "levels + atlas packing (numpy oracle port of ctprev, process pool over blocks of slices x row bands)",
                "seconds": c_s}
         _CPU_VOL = None
 
