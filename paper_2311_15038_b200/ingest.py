@@ -123,3 +123,108 @@ def preview_from_raw(header_path, schemes=(512, 256, 128), n_top: int = 3, frac:
     flags = out["flags"].numpy()
     return PreviewResult(out["hist"].numpy().copy(), frozenset(int(b) for b in np.nonzero(flags)[0]), slicemaps,
                          {}, None)
+
+
+# ---------------------------------------------------------------------------
+# slice stacks (volume.py:167-202 load_slice_stack): a JSON manifest listing one
+# 8-bit grayscale PNG per z slice.  The reference decodes every slice serially
+# into one host array; here the manifest is validated as load_slice_stack does
+# (same checks, same error classes), and the slices are decoded by a thread pool
+# (Pillow releases the GIL while decoding) straight into the pinned chunk ring of
+# PreviewSession.run_reader, so decoding chunk c+1 overlaps chunk c's H2D copy
+# and fused pass and no whole-volume host array exists.
+
+def _open_slice(path: Path):
+    from PIL import Image
+    if not path.is_file():
+        raise MissingSlice(str(path))                      # volume.py:157-158
+    im = Image.open(path)
+    if im.mode != "L":                                     # volume.py:160-163
+        im.close()
+        raise UnsupportedPixelFormat(f"{path.name}: mode {im.mode!r}, need 8-bit grayscale ('L')")
+    return im
+
+
+def read_manifest(manifest_path) -> tuple[list, tuple[int, int, int]]:
+    """volume.py:176-196: (slice paths in z order, (nz, ny, nx)) or the reference's error."""
+    manifest_path = Path(manifest_path)
+    try:
+        manifest = json.loads(manifest_path.read_text())
+    except (OSError, json.JSONDecodeError) as exc:
+        raise InvalidManifest(f"{manifest_path}: {exc}") from exc
+    if not isinstance(manifest, dict) or "slices" not in manifest:
+        raise InvalidManifest(f"{manifest_path}: no 'slices' key")
+    if manifest.get("bit_depth", 8) != 8:
+        raise UnsupportedPixelFormat(f"bit_depth {manifest.get('bit_depth')}, only 8 is supported")
+    rel = manifest["slices"]
+    if not isinstance(rel, list) or len(rel) == 0:
+        raise InvalidManifest(f"{manifest_path}: manifest lists no slices")
+    paths = [manifest_path.parent / name for name in rel]
+    with _open_slice(paths[0]) as im:
+        nx, ny = im.size
+    return paths, (len(paths), ny, nx)
+
+
+class SliceStackReader:
+    """``read(z0, z1, out)`` for PreviewSession.run_reader: decodes slices [z0, z1)
+    of a stack into ``out`` with ``threads`` concurrent Pillow decodes; every slice
+    is checked against the first slice's size (volume.py:197-201)."""
+
+    def __init__(self, paths, shape, threads: int = 8):
+        from concurrent.futures import ThreadPoolExecutor
+        self.paths = list(paths)
+        self.shape = tuple(shape)
+        self._pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
+
+    def _decode(self, z: int, dst: np.ndarray) -> None:
+        path = self.paths[z]
+        with _open_slice(path) as im:
+            if (im.size[1], im.size[0]) != self.shape[1:]:
+                raise DimensionMismatch(f"slice {path.name}: {im.size} does not match first slice "
+                                        f"{(self.shape[2], self.shape[1])}")
+            dst[...] = np.asarray(im, dtype=np.uint8)
+
+    def __call__(self, z0: int, z1: int, out: np.ndarray) -> None:
+        if self._pool is None:
+            for z in range(z0, z1):
+                self._decode(z, out[z - z0])
+            return
+        for f in [self._pool.submit(self._decode, z, out[z - z0]) for z in range(z0, z1)]:
+            f.result()
+
+    def close(self) -> None:
+        if self._pool is not None:
+            self._pool.shutdown()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def preview_from_slice_stack(manifest_path, schemes=(512, 256, 128), n_top: int = 3, frac: float = 0.0005,
+                             chunk_slices: int = 64, session: PreviewSession | None = None, threads: int = 8):
+    """``preview_pipeline(load_slice_stack(manifest_path), schemes)`` with the slices
+    decoded in parallel straight into the streaming pass: returns the same
+    ``PreviewResult`` (histogram, artifact bins, per-scheme SlicemapSets)."""
+    from .ops import PreviewResult
+    paths, shape = read_manifest(manifest_path)
+    sch = {}
+    for sc in schemes:
+        sc = plan_scheme(sc) if isinstance(sc, int) else sc
+        sch[sc.s] = sc
+    if session is None:
+        session = PreviewSession(shape, torch.uint8, {s: AtlasSpec.of(sc) for s, sc in sch.items()}, n_top=n_top,
+                                 frac=frac, chunk_slices=chunk_slices)
+    elif session.shape != shape:
+        raise DimensionMismatch(f"session shape {session.shape} != stack {shape}")
+    with SliceStackReader(paths, shape, threads=threads) as rd:
+        out = session.run_reader(rd)
+    slicemaps = {}
+    for s, sc in sch.items():
+        a = out["atlases"][s].numpy()
+        slicemaps[s] = FACTORY.SlicemapSet(scheme=sc, atlases=tuple(a[m].copy() for m in range(sc.map_count)))
+    flags = out["flags"].numpy()
+    return PreviewResult(out["hist"].numpy().copy(), frozenset(int(b) for b in np.nonzero(flags)[0]), slicemaps,
+                         {}, None)

@@ -139,3 +139,126 @@ def test_preview_session_host_buffers_equal_in_memory(cuda, u16):
         assert frozenset(np.nonzero(out["flags"].numpy())[0].tolist()) == ref.bins
         for s in (256, 128):
             assert np.array_equal(out["atlases"][s].numpy(), np.stack(ref.slicemaps[s].atlases)), (it, s)
+
+
+# ---------------------------------------------------------------- slice stacks (volume.py:167-202)
+
+def _write_stack(tmp, vol, name="stack", manifest=None, mode="L"):
+    from PIL import Image
+    files = []
+    for z in range(vol.shape[0]):
+        f = f"{name}_{z:04d}.png"
+        im = Image.fromarray(vol[z])
+        (im if mode == "L" else im.convert(mode)).save(tmp / f)
+        files.append(f)
+    m = {"name": name, "slices": files, "bit_depth": 8} if manifest is None else manifest
+    (tmp / f"{name}.json").write_text(m if isinstance(m, str) else json.dumps(m))
+    return tmp / f"{name}.json"
+
+
+def test_slice_stack_manifest_errors_and_reader(tmp_path):
+    """read_manifest / SliceStackReader raise load_slice_stack's error classes under
+    its conditions and decode the slices in z order."""
+    from paper_2311_15038_b200 import errors as E
+    from paper_2311_15038_b200.ingest import SliceStackReader, read_manifest
+    rng = np.random.default_rng(3)
+    vol = rng.integers(0, 256, size=(5, 7, 9), dtype=np.uint8)
+    ok = _write_stack(tmp_path, vol)
+    paths, shape = read_manifest(ok)
+    assert shape == (5, 7, 9) and len(paths) == 5
+    out = np.zeros((3, 7, 9), dtype=np.uint8)
+    with SliceStackReader(paths, shape, threads=4) as rd:
+        rd(1, 4, out)
+    assert np.array_equal(out, vol[1:4])
+    (tmp_path / "bad.json").write_text("{not json")
+    with pytest.raises(E.InvalidManifest):
+        read_manifest(tmp_path / "bad.json")
+    (tmp_path / "noslices.json").write_text(json.dumps({"name": "x"}))
+    with pytest.raises(E.InvalidManifest):
+        read_manifest(tmp_path / "noslices.json")
+    (tmp_path / "empty.json").write_text(json.dumps({"slices": []}))
+    with pytest.raises(E.InvalidManifest):
+        read_manifest(tmp_path / "empty.json")
+    (tmp_path / "deep.json").write_text(json.dumps({"slices": ["stack_0000.png"], "bit_depth": 16}))
+    with pytest.raises(E.UnsupportedPixelFormat):
+        read_manifest(tmp_path / "deep.json")
+    (tmp_path / "gone.json").write_text(json.dumps({"slices": ["nope.png"]}))
+    with pytest.raises(E.MissingSlice):
+        read_manifest(tmp_path / "gone.json")
+    rgb = _write_stack(tmp_path, vol[:2], name="rgb", mode="RGB")
+    with pytest.raises(E.UnsupportedPixelFormat):
+        read_manifest(rgb)
+    from PIL import Image
+    Image.fromarray(np.zeros((8, 9), np.uint8)).save(tmp_path / "odd.png")
+    (tmp_path / "mixed.json").write_text(json.dumps({"slices": ["stack_0000.png", "odd.png"]}))
+    paths, shape = read_manifest(tmp_path / "mixed.json")
+    with pytest.raises(E.DimensionMismatch):
+        with SliceStackReader(paths, shape, threads=2) as rd:
+            rd(0, 2, np.zeros((2, 7, 9), np.uint8))
+
+
+@pytest.mark.gpu
+def test_preview_from_slice_stack_equals_in_memory(cuda, tmp_path):
+    """A PNG slice stack decoded in parallel straight into the streaming pass (chunks
+    of 32 slices) == preview_pipeline on the assembled volume."""
+    import paper_2311_15038_b200 as P
+    from paper_2311_15038_b200.ingest import preview_from_slice_stack
+    rng = np.random.default_rng(9)
+    vol = np.clip(np.rint(rng.normal(25, 7, (96, 128, 128))), 0, 255).astype(np.uint8)
+    vol[20:70, 30:90, 40:100] = rng.integers(120, 220, size=(50, 60, 60), dtype=np.uint8)
+    vol[-3:, :40] = 150
+    man = _write_stack(tmp_path, vol)
+    got = preview_from_slice_stack(man, schemes=(128, P.SlicemapScheme(64, 512, 8, 1)), chunk_slices=32)
+    ref = P.preview_pipeline(vol, schemes=(128, P.SlicemapScheme(64, 512, 8, 1)))
+    assert np.array_equal(got.histogram, ref.histogram)
+    assert got.bins == ref.bins
+    for s in (128, 64):
+        assert np.array_equal(np.stack(got.slicemaps[s].atlases), np.stack(ref.slicemaps[s].atlases)), s
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not mounted")
+def test_slice_stack_errors_match_load_slice_stack(tmp_path):
+    """Same error class names as the reference's load_slice_stack (volume.py:167-202)
+    for every bad-manifest / bad-slice case, and the same volume for a good stack."""
+    import subprocess
+    import sys
+    from PIL import Image
+    rng = np.random.default_rng(4)
+    vol = rng.integers(0, 256, size=(4, 6, 10), dtype=np.uint8)
+    cases = {"ok": _write_stack(tmp_path, vol)}
+    (tmp_path / "bad.json").write_text("{not json")
+    cases["json"] = tmp_path / "bad.json"
+    (tmp_path / "noslices.json").write_text(json.dumps({"name": "x"}))
+    cases["noslices"] = tmp_path / "noslices.json"
+    (tmp_path / "empty.json").write_text(json.dumps({"slices": []}))
+    cases["empty"] = tmp_path / "empty.json"
+    (tmp_path / "deep.json").write_text(json.dumps({"slices": ["stack_0000.png"], "bit_depth": 16}))
+    cases["deep"] = tmp_path / "deep.json"
+    (tmp_path / "gone.json").write_text(json.dumps({"slices": ["stack_0000.png", "nope.png"]}))
+    cases["gone"] = tmp_path / "gone.json"
+    cases["rgb"] = _write_stack(tmp_path, vol[:2], name="rgb", mode="RGB")
+    Image.fromarray(np.zeros((8, 9), np.uint8)).save(tmp_path / "odd.png")
+    (tmp_path / "mixed.json").write_text(json.dumps({"slices": ["stack_0000.png", "odd.png"]}))
+    cases["mixed"] = tmp_path / "mixed.json"
+    code = ("import sys, json; sys.path.insert(0, %r)\n"
+            "from ctprev.volume import load_slice_stack\n"
+            "out = {}\n"
+            "for k, p in json.loads(sys.argv[1]).items():\n"
+            "    try:\n        v = load_slice_stack(p); out[k] = int(v.voxels.astype('int64').sum())\n"
+            "    except Exception as e:\n        out[k] = type(e).__name__\n"
+            "print(json.dumps(out))\n") % str(REF)
+    r = subprocess.run([sys.executable, "-c", code, json.dumps({k: str(p) for k, p in cases.items()})],
+                       capture_output=True, text=True, env={"NUMBA_CACHE_DIR": "/tmp/numba_cache_ingest",
+                                                            "PYTHONDONTWRITEBYTECODE": "1", "PATH": "/usr/bin"})
+    ref = json.loads(r.stdout.strip().splitlines()[-1])
+    from paper_2311_15038_b200.ingest import SliceStackReader, read_manifest
+    for k, p in cases.items():
+        try:
+            paths, shape = read_manifest(p)
+            out = np.zeros(shape, np.uint8)
+            with SliceStackReader(paths, shape, threads=2) as rd:
+                rd(0, shape[0], out)
+            got = int(out.astype(np.int64).sum())
+        except Exception as e:
+            got = type(e).__name__
+        assert got == ref[k], (k, got, ref[k])
