@@ -20,8 +20,8 @@ from .types import (ADDITIVE, ALPHA, MIP, SURFACE, EntropyResult, Histogram256, 
 from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, build_interactive_preview,
                   build_list_preview,
                   decode_slicemaps, downscale_volume, encode_slicemaps, save_slicemaps,
-                  filter_histogram_bins, image_entropy, optimal_snapshot, preview_pipeline, render_view,
-                  render_views, volume_histogram)
+                  filter_histogram_bins, image_entropy, load_slice_stack, optimal_snapshot, preview_pipeline,
+                  render_view, render_views, volume_histogram)
 from .install import install, uninstall
 
 __version__ = "0.1.0"
@@ -33,5 +33,5 @@ __all__ = [
     "decode_slicemaps", "render_view", "render_views", "image_entropy", "optimal_snapshot",
     "preview_pipeline", "PreviewResult", "build_data_preview", "build_interactive_preview", "build_list_preview",
     "apply_circle_mask",
-    "save_slicemaps", "install", "uninstall",
+    "save_slicemaps", "load_slice_stack", "install", "uninstall",
 ]

@@ -30,6 +30,7 @@ BINDINGS = {
     "build_interactive_preview": ["pipeline", ""],
     "build_list_preview": ["pipeline", ""],
     "save_slicemaps": ["slicemap", "pipeline", ""],
+    "load_slice_stack": ["volume", "pipeline", ""],
 }
 
 _saved: dict = {}

@@ -457,3 +457,17 @@ def build_interactive_preview(volume, detect=None, threshold=None, margin: float
 
 
 from .png import save_slicemaps  # noqa: E402,F401  (slicemap.py:158-166, device filter + parallel deflate)
+
+
+def load_slice_stack(manifest_path, threads: int = 8):
+    """volume.py:167-202 drop-in: the same manifest checks and error classes, the
+    slices decoded by a thread pool (Pillow releases the GIL while decoding) into
+    one C-contiguous (nz, ny, nx) uint8 array, returned as the reference's Volume.
+    Host I/O only -- the device path streams a stack with
+    ``ingest.preview_from_slice_stack`` instead of materialising it."""
+    from .ingest import SliceStackReader, read_manifest
+    paths, shape = read_manifest(manifest_path)
+    stack = np.empty(shape, dtype=np.uint8)
+    with SliceStackReader(paths, shape, threads=threads) as rd:
+        rd(0, shape[0], stack)
+    return FACTORY.Volume(stack)

@@ -140,6 +140,7 @@ def test_install_rebinds_every_site(monkeypatch, tmp_path):
         assert ctprev.slicemap.downscale_volume is P.downscale_volume
         assert ctprev.render.render_view is P.render_view
         assert ctprev.volume_histogram is P.volume_histogram
+        assert ctprev.pipeline.load_slice_stack is P.load_slice_stack
         from paper_2311_15038_b200.types import FACTORY
         assert FACTORY.Volume is ctprev.volume.Volume and FACTORY.SlicemapSet is ctprev.slicemap.SlicemapSet
     finally:

@@ -185,6 +185,9 @@ def test_slice_stack_manifest_errors_and_reader(tmp_path):
     (tmp_path / "gone.json").write_text(json.dumps({"slices": ["nope.png"]}))
     with pytest.raises(E.MissingSlice):
         read_manifest(tmp_path / "gone.json")
+    import paper_2311_15038_b200 as P
+    v = P.load_slice_stack(ok, threads=3)            # the host drop-in (volume.py:167-202)
+    assert np.array_equal(v.voxels, vol) and v.voxels.flags["C_CONTIGUOUS"]
     rgb = _write_stack(tmp_path, vol[:2], name="rgb", mode="RGB")
     with pytest.raises(E.UnsupportedPixelFormat):
         read_manifest(rgb)
