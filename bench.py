@@ -753,6 +753,41 @@ def bench_other_configs(device):
                                 "ms_per_volume": min(ts) * 1e3, "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9,
                                 "host_bytes_held": 3 * 64 * ny * nx + 3 * ny * nx}
 
+    def _c2_stack():
+        # ingest from a PNG slice stack (load_slice_stack's manifest format, volume.py:167-202): parallel
+        # decode straight into the streaming pass; the stack is written to a temp dir
+        import tempfile
+        from concurrent.futures import ThreadPoolExecutor
+        from PIL import Image
+        from paper_2311_15038_b200.ingest import preview_from_slice_stack
+        from paper_2311_15038_b200.pipeline import PreviewSession
+        from paper_2311_15038_b200.device import AtlasSpec as _AS
+        spec = synth.config("c2")
+        v = synth.generate(spec, device=device).cpu().numpy()
+        nz, ny, nx = spec.shape
+        threads = os.cpu_count() or 8
+        with tempfile.TemporaryDirectory() as td:
+            names = [f"s_{z:04d}.png" for z in range(nz)]
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(lambda z: Image.fromarray(v[z]).save(os.path.join(td, names[z]), compress_level=1),
+                            range(nz)))
+            del v
+            with open(os.path.join(td, "stack.json"), "w") as f:
+                json.dump({"name": "c2", "slices": names, "bit_depth": 8}, f)
+            sess = PreviewSession(spec.shape, torch.uint8, {s: _AS.of(plan_scheme(s)) for s in (512, 256, 128)})
+            man = os.path.join(td, "stack.json")
+            preview_from_slice_stack(man, session=sess, threads=threads)
+            ts = []
+            for _ in range(2):
+                t0 = time.perf_counter()
+                preview_from_slice_stack(man, session=sess, threads=threads)
+                ts.append(time.perf_counter() - t0)
+            del sess
+        out["c2_stack_ingest"] = {"workload": "c2 as 1024 PNG slices + manifest (volume.py:167-202 format): manifest "
+                                              "checks, parallel decode into pinned chunks overlapped with H2D + "
+                                              "fused pass, atlases back to host", "ms_per_volume": min(ts) * 1e3,
+                                  "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9, "decode_threads": threads}
+
     def _c2_png():
         # atlas PNG writing: the c2 step's 14 atlases (8 x 4096^2 + 4 x 2048^2 + 2 x 1024^2)
         # as save_slicemaps writes them -- device filter + parallel deflate vs Pillow (slicemap.py:164)
@@ -791,7 +826,7 @@ def bench_other_configs(device):
 
 
     for name, fn in (("c1", _c1), ("c3", _c3), ("c4_alpha", _c4_alpha), ("c5", _c5), ("c2_ingest", _c2_ingest),
-                     ("c2_png", _c2_png)):
+                     ("c2_stack_ingest", _c2_stack), ("c2_png", _c2_png)):
         try:  # one side measurement failing (e.g. memory) must not cost the bench line
             fn()
         except Exception as e:  # pragma: no cover - reported in the JSON line
