@@ -20,7 +20,7 @@ from .types import (ADDITIVE, ALPHA, MIP, SURFACE, EntropyResult, Histogram256, 
 from .ops import (PreviewResult, apply_circle_mask, artifact_bins, build_data_preview, build_interactive_preview,
                   build_list_preview,
                   decode_slicemaps, downscale_volume, encode_slicemaps, save_slicemaps,
-                  filter_histogram_bins, image_entropy, load_slice_stack, optimal_snapshot, preview_pipeline,
+                  filter_histogram_bins, image_entropy, load_slice_stack, load_volume, optimal_snapshot, preview_pipeline,
                   render_view, render_views, volume_histogram)
 from .install import install, uninstall
 
@@ -33,5 +33,5 @@ __all__ = [
     "decode_slicemaps", "render_view", "render_views", "image_entropy", "optimal_snapshot",
     "preview_pipeline", "PreviewResult", "build_data_preview", "build_interactive_preview", "build_list_preview",
     "apply_circle_mask",
-    "save_slicemaps", "load_slice_stack", "install", "uninstall",
+    "save_slicemaps", "load_slice_stack", "load_volume", "install", "uninstall",
 ]

@@ -31,6 +31,7 @@ BINDINGS = {
     "build_list_preview": ["pipeline", ""],
     "save_slicemaps": ["slicemap", "pipeline", ""],
     "load_slice_stack": ["volume", "pipeline", ""],
+    "load_volume": ["volume", "pipeline", "cli", ""],
 }
 
 _saved: dict = {}

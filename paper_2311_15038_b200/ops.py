@@ -459,6 +459,20 @@ def build_interactive_preview(volume, detect=None, threshold=None, margin: float
 from .png import save_slicemaps  # noqa: E402,F401  (slicemap.py:158-166, device filter + parallel deflate)
 
 
+def load_volume(header_path, threads: int = 8):
+    """volume.py:229-249 drop-in: the header checked exactly as load_volume does
+    (same order, error classes and messages), the raw bytes read by ``threads``
+    concurrent preadv calls into one (nz, ny, nx) uint8 array, returned as the
+    reference's Volume with its voxel size.  Host I/O only -- the device path
+    streams a raw volume with ``ingest.preview_from_raw`` instead."""
+    from .ingest import RawReader, read_header
+    shape, raw, voxel_size = read_header(header_path)
+    arr = np.empty(shape, dtype=np.uint8)
+    with RawReader(raw, shape, threads=threads) as rd:
+        rd(0, shape[0], arr)
+    return FACTORY.Volume(arr, voxel_size)
+
+
 def load_slice_stack(manifest_path, threads: int = 8):
     """volume.py:167-202 drop-in: the same manifest checks and error classes, the
     slices decoded by a thread pool (Pillow releases the GIL while decoding) into

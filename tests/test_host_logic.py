@@ -135,12 +135,13 @@ def test_install_rebinds_every_site(monkeypatch, tmp_path):
     try:
         patched = inst.install()
         assert "ctprev.pipeline.encode_slicemaps" in patched and "ctprev.slicemap.downscale_volume" in patched
-        import ctprev.mask, ctprev.pipeline, ctprev.render, ctprev.slicemap, ctprev.volume  # noqa: E401
+        import ctprev.cli, ctprev.mask, ctprev.pipeline, ctprev.render, ctprev.slicemap, ctprev.volume  # noqa: E401
         assert ctprev.pipeline.volume_histogram is P.volume_histogram
         assert ctprev.slicemap.downscale_volume is P.downscale_volume
         assert ctprev.render.render_view is P.render_view
         assert ctprev.volume_histogram is P.volume_histogram
         assert ctprev.pipeline.load_slice_stack is P.load_slice_stack
+        assert ctprev.cli.load_volume is P.load_volume
         from paper_2311_15038_b200.types import FACTORY
         assert FACTORY.Volume is ctprev.volume.Volume and FACTORY.SlicemapSet is ctprev.slicemap.SlicemapSet
     finally:

@@ -46,6 +46,13 @@ def test_read_header_errors(tmp_path):
     vol = np.zeros((5, 6, 7), dtype=np.uint8)
     shape, raw, vs = read_header(_write(tmp_path, "ok", vol))
     assert shape == (5, 6, 7) and raw.name == "ok.raw" and vs == 1.5
+    import paper_2311_15038_b200 as P
+    rnd = np.random.default_rng(2).integers(0, 256, size=(9, 6, 7), dtype=np.uint8)
+    v = P.load_volume(_write(tmp_path, "rnd", rnd), threads=3)   # the host drop-in (volume.py:229-249)
+    assert np.array_equal(v.voxels, rnd) and v.voxel_size_um == 1.5
+    for k, p in _bad_headers(tmp_path).items():
+        with pytest.raises(want[k]):
+            P.load_volume(p)
 
 
 @pytest.mark.skipif(not REF.exists(), reason="reference not mounted")
