@@ -60,8 +60,14 @@ typedef struct ctp_level_out {
   int32_t grid;        /* atlas: cells per atlas row */
   int32_t atlas_dim;   /* atlas: grid * s */
   int32_t map_count;   /* atlas: number of maps */
-  int32_t _pad;
+  int32_t flags;       /* CTP_OUT_PEER: `out` is another GPU's memory (ctp_ipc_import) */
 } ctp_level_out;
+
+/* Output flag: the destination is a peer GPU's buffer mapped through CUDA IPC.
+ * Kernels writing there end with a system-scope fence (__threadfence_system),
+ * so their stores are visible to the peer before any later signal issued on
+ * the same stream (the collective that completes a sharded step). */
+#define CTP_OUT_PEER 1
 
 #define CTP_MAX_LEVELS 5  /* level 0 (full res) .. level 4 (16:1) */
 
@@ -219,11 +225,12 @@ int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx,
  * [floor(uz)-2, floor(uz)+3]), else CTP_E_INVALID.  View q's band is written
  * at out + q * out_view_stride (0 = packed bands); with `out` pointing at row
  * row0 of a full-image buffer (stride = image bytes) -- e.g. rank 0's images
- * mapped through ctp_ipc_import -- the sort-last composite is the render. */
+ * mapped through ctp_ipc_import, out_flags = CTP_OUT_PEER) -- the sort-last
+ * composite is the render. */
 int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz,
                        int64_t nz, int64_t ny, int64_t nx,
                        const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1,
-                       uint8_t* out, int64_t out_view_stride, void* stream);
+                       uint8_t* out, int64_t out_view_stride, int32_t out_flags, void* stream);
 
 /* The fp32 MIP/alpha path keeps its per-row planes (2 B per voxel per image
  * row) allocated between calls while the shape is unchanged; this frees them. */

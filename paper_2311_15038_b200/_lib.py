@@ -20,6 +20,7 @@ CTP_E_ALIGN = -4
 
 LAYOUT_XYZ = 0
 LAYOUT_ATLAS = 1
+OUT_PEER = 1  # ctp_level_out.flags / out_flags: destination mapped from a peer GPU
 MAX_LEVELS = 5
 
 MODE_SURFACE, MODE_ADDITIVE, MODE_MIP, MODE_ALPHA = 0, 1, 2, 3
@@ -46,7 +47,7 @@ class LevelOut(C.Structure):
         ("grid", C.c_int32),
         ("atlas_dim", C.c_int32),
         ("map_count", C.c_int32),
-        ("_pad", C.c_int32),
+        ("flags", C.c_int32),   # OUT_PEER: a peer GPU's memory (ctp_ipc_import)
     ]
 
 
@@ -90,7 +91,7 @@ SIGNATURES = {
     "ctp_decode_atlas_u8": [_P, _I32, _I32, _I32, _I32, _P, _P],
     "ctp_circle_mask_u8": [_P, _I64, _I64, _I64, C.c_double, C.c_double, C.c_double, _P, _P],
     "ctp_render_u8": [_P, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _P],
-    "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _I64, _P],
+    "ctp_render_slab_u8": [_P, _I64, _I64, _I64, _I64, _I64, C.POINTER(View), _I32, _I64, _I64, _P, _I64, _I32, _P],
     "ctp_render_release": [],
     "ctp_png_filter_u8": [_P, _I32, _I64, _I64, _I32, _P, _P],
     "ctp_deflate_geometry": [C.POINTER(_I32), C.POINTER(_I32)],

@@ -86,6 +86,7 @@ struct PvArgs {
   uint8_t* lut_out;                // optional copies for the host
   uint8_t* flags_out;
   unsigned long long* ws;          // uint64[4097], zero on entry, left zero
+  int32_t fence_sys;               // a level destination is a peer GPU's memory (CTP_OUT_PEER)
 };
 
 // ---- PTX helpers -------------------------------------------------------------
@@ -586,6 +587,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   flush_counts<T>(hs, a.hist, THREADS);
+  // atlas rows stored into a peer's atlases (the fused gather of a sharded step):
+  // system-scope fence, so they are visible to the peer before the collective that
+  // follows this kernel on the stream completes the step
+  if (a.fence_sys) __threadfence_system();
 #ifdef CTP_PHASE_TIMING
   if ((blockIdx.x == 0 || blockIdx.x == gridDim.x / 2) && (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) % 8 == 0)
     printf("PHASE cta %d warp %2d tiles %d total %lld  data-wait %lld  units %lld  barrier %lld  levels+refill %lld\n",
@@ -821,6 +826,9 @@ static int preview_impl(const T* vol, int64_t nz, int64_t ny, int64_t nx, int64_
   a.vmax = 0;
   a.lut_out = a.flags_out = nullptr;
   a.ws = nullptr;
+  a.fence_sys = 0;
+  for (int l = 0; l <= nlev; l++)
+    if (levels[l].out != nullptr && (levels[l].flags & CTP_OUT_PEER)) a.fence_sys = 1;
   if (autolut != nullptr) {
     CTP_REQUIRE(1 <= autolut->n_top && autolut->n_top <= nz, CTP_E_INVALID, "n_top %d outside [1, %lld]",
                 autolut->n_top, (long long)nz);  // mask.py:223-224

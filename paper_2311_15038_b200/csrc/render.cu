@@ -42,6 +42,7 @@ constexpr int kMaxViews = 64;
 struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per launch
   ViewDev v[kMaxViews];
   int64_t vstride;  // bytes between consecutive views' first rows in `out`
+  int32_t peer;     // `out` is a peer GPU's memory: system-scope fence after the stores
 };
 
 // 2x2 footprint of one slice of a layered u8 texture (clamp addressing): the
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(128, CTP_RENDER_MINB) render_kernel(const uint
       dst[0] = to_u8_unit<R>(A);
     }
   }
+  if (views.peer) __threadfence_system();  // stores into a peer's images: visible before the completing collective
 }
 
 
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
                                                               to_u8_unit<float>(C2), to_u8_unit<float>(A));
     else dst[0] = to_u8_unit<float>(A);
   }
+  if (views.peer) __threadfence_system();
 }
 
 // Row planes: every image row j of the turntable lives at one z (render.py:140),
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t te
                                                               to_u8_unit<float>(C2), to_u8_unit<float>(A));
     else dst[0] = to_u8_unit<float>(A);
   }
+  if (views.peer) __threadfence_system();
 }
 
 struct RowPlanes {
@@ -707,8 +711,9 @@ static void row_slices(int64_t j, double big_r, double px_size, double n_max, in
 
 static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, int64_t ny, int64_t nx,
                        const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out,
-                       int64_t vstride, void* stream) {
+                       int64_t vstride, int32_t out_flags, void* stream) {
   CTP_REQUIRE(vol && views && out, CTP_E_INVALID, "ctp_render_u8: null pointer");
+  CTP_REQUIRE((out_flags & ~CTP_OUT_PEER) == 0, CTP_E_INVALID, "unknown out_flags %d", out_flags);
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1 && nx < (1LL << 31) && ny < (1LL << 31) && nz < (1LL << 31),
               CTP_E_INVALID, "ctp_render_u8: bad shape");
   CTP_REQUIRE(0 <= zb && snz >= 1 && zb + snz <= nz, CTP_E_INVALID, "slab [%lld, %lld) outside [0, %lld)",
@@ -782,6 +787,7 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
   CTP_REQUIRE(vstride == 0 || vstride >= band, CTP_E_INVALID, "out_view_stride %lld below one band (%lld bytes)",
               (long long)vstride, (long long)band);
   vb.vstride = vstride ? vstride : band;
+  vb.peer = (out_flags & CTP_OUT_PEER) ? 1 : 0;
   dim3 grid((dim + 127) / 128, (unsigned)(row1 - row0), (unsigned)n_views);
   const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && snz <= 2048 &&
                         nx <= 32768 && ny <= 32768;
@@ -876,13 +882,14 @@ extern "C" {
 
 int ctp_render_u8(const uint8_t* vol, int64_t nz, int64_t ny, int64_t nx, const ctp_view* views, int32_t n_views,
                   int64_t row0, int64_t row1, uint8_t* out, void* stream) {
-  return render_impl(vol, 0, nz, nz, ny, nx, views, n_views, row0, row1, out, 0, stream);
+  return render_impl(vol, 0, nz, nz, ny, nx, views, n_views, row0, row1, out, 0, 0, stream);
 }
 
 int ctp_render_slab_u8(const uint8_t* slab, int64_t z_base, int64_t slab_nz, int64_t nz, int64_t ny, int64_t nx,
                        const ctp_view* views, int32_t n_views, int64_t row0, int64_t row1, uint8_t* out,
-                       int64_t out_view_stride, void* stream) {
-  return render_impl(slab, z_base, slab_nz, nz, ny, nx, views, n_views, row0, row1, out, out_view_stride, stream);
+                       int64_t out_view_stride, int32_t out_flags, void* stream) {
+  return render_impl(slab, z_base, slab_nz, nz, ny, nx, views, n_views, row0, row1, out, out_view_stride, out_flags,
+                     stream);
 }
 
 int ctp_render_release(void) {

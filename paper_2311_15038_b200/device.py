@@ -181,6 +181,11 @@ def alloc_level(level_shape, spec, device, zero_pad: bool = True):
     return torch.zeros(shape, dtype=torch.uint8, device=device)
 
 
+def _out_flags(t) -> int:
+    """OUT_PEER for a destination mapped from another GPU (``dist.PeerBuffer``)."""
+    return _lib.OUT_PEER if getattr(t, "is_peer", False) else 0
+
+
 def preview(vol: torch.Tensor, lut: torch.Tensor | None, outputs: dict, hist: torch.Tensor | None = None,
             z_base: int = 0, full_nz: int | None = None, out_tensors: dict | None = None):
     """ONE pass: hist(vol) += ..., f = lut[vol], levels l in ``outputs`` (l -> "xyz" | AtlasSpec).
@@ -201,10 +206,10 @@ def preview(vol: torch.Tensor, lut: torch.Tensor | None, outputs: dict, hist: to
             t = alloc_level(shape, spec, vol.device)
         res[l] = t
         if spec is None or spec == "xyz":
-            levels[l] = LevelOut(t.data_ptr(), _lib.LAYOUT_XYZ, 0, 0, 0, 0, 0)
+            levels[l] = LevelOut(t.data_ptr(), _lib.LAYOUT_XYZ, 0, 0, 0, 0, _out_flags(t))
         else:
             levels[l] = LevelOut(t.data_ptr(), _lib.LAYOUT_ATLAS, spec.s, spec.grid, spec.atlas_dim,
-                                 spec.map_count, 0)
+                                 spec.map_count, _out_flags(t))
     arr = _lib.levels_array(levels)
     fn = "ctp_preview_u16" if is16 else "ctp_preview_u8"
     _lib.call(fn, _ptr(vol), nz, ny, nx, z_base, _ptr(lut), nlev, arr, _ptr(hist), _stream())
@@ -270,7 +275,7 @@ def make_view(p, channels: int = 1, fp32: bool = False) -> View:
 
 def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False, rows=None,
            out: torch.Tensor | None = None, z_base: int = 0, full_nz: int | None = None,
-           out_ptr: int | None = None, out_view_stride: int = 0) -> torch.Tensor | None:
+           out_ptr: int | None = None, out_view_stride: int = 0, out_peer: bool = False) -> torch.Tensor | None:
     """render.py:205-236, batched over views (<= 64 per launch).
     Returns uint8 (n, rows, dim) or (n, rows, dim, 4).
 
@@ -278,7 +283,8 @@ def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False
     ``full_nz`` deep): the geometry is the full volume's and every requested row
     must read only held slices (``dist.row_slices``), else the library refuses.
     ``out_ptr`` / ``out_view_stride``: write view q's band at out_ptr + q * stride
-    instead (e.g. into rank 0's full images through a peer mapping); returns None."""
+    instead (e.g. into rank 0's full images through a peer mapping, ``out_peer``:
+    the kernels then end with a system-scope fence); returns None."""
     _check_dev(vol, torch.uint8, "render")
     snz, ny, nx = vol.shape
     nz = snz if full_nz is None else int(full_nz)
@@ -298,11 +304,11 @@ def render(vol: torch.Tensor, params_list, channels: int = 1, fp32: bool = False
         chunk = params_list[b:b + 64]
         arr = (View * len(chunk))(*[make_view(p, channels, fp32) for p in chunk])
         dst = C.c_void_p(base + b * stride)
-        if z_base == 0 and snz == nz and stride == band:
+        if z_base == 0 and snz == nz and stride == band and not out_peer:
             _lib.call("ctp_render_u8", _ptr(vol), nz, ny, nx, arr, len(chunk), r0, r1, dst, _stream())
         else:
             _lib.call("ctp_render_slab_u8", _ptr(vol), z_base, snz, nz, ny, nx, arr, len(chunk), r0, r1, dst,
-                      stride, _stream())
+                      stride, _lib.OUT_PEER if out_peer else 0, _stream())
     return out if out_ptr is None else None
 
 

@@ -66,6 +66,8 @@ class PeerBuffer:
     """A device buffer of another process of the node, mapped through CUDA IPC
     (``ctp_ipc_import``); usable wherever the kernels take a destination pointer."""
 
+    is_peer = True  # kernels storing here end with a system-scope fence (CTP_OUT_PEER)
+
     def __init__(self, handle: bytes, offset: int, shape, dtype=torch.uint8):
         import ctypes as C
         from . import _lib
@@ -208,9 +210,16 @@ class ShardedPreview:
             else:
                 lut = self.compute.artifact_lut(top, self.n_top, self.frac)
         else:
-            lut = torch.empty(self.compute.nbins, dtype=torch.uint8, device=self.device)
+            lut = torch.zeros(self.compute.nbins, dtype=torch.uint8, device=self.device)
         if self.world > 1:
-            dist.broadcast(lut, src=owner, group=self.group)
+            if self.peer:
+                # peer mode: every rank's pass stores into rank 0's atlases, which are reused by
+                # every step -- so the LUT is distributed by an all-reduce (MAX over the owner's
+                # LUT and zeros) instead of a broadcast: no rank can start its pass before rank 0
+                # has entered this step, i.e. finished with the previous step's atlases
+                dist.all_reduce(lut, op=dist.ReduceOp.MAX, group=self.group)
+            else:
+                dist.broadcast(lut, src=owner, group=self.group)
         if not zeroed:
             self.hist.zero_()
         if self.fused_events is not None:
@@ -324,11 +333,12 @@ class DeviceRenderCompute(RenderCompute):
     def render(self, slab, z_base, full_nz, views, rows, channels, fp32):
         return self.dev.render(slab, views, channels=channels, fp32=fp32, rows=rows, z_base=z_base, full_nz=full_nz)
 
-    def render_into(self, slab, z_base, full_nz, views, rows, channels, fp32, out_ptr: int, view_stride: int):
+    def render_into(self, slab, z_base, full_nz, views, rows, channels, fp32, out_ptr: int, view_stride: int,
+                    peer: bool = True):
         """Write each view's row band straight into full images at ``out_ptr`` (row 0 of view 0)."""
         d = int(views[0].image_dim)
         self.dev.render(slab, views, channels=channels, fp32=fp32, rows=rows, z_base=z_base, full_nz=full_nz,
-                        out_ptr=out_ptr + rows[0] * d * channels, out_view_stride=view_stride)
+                        out_ptr=out_ptr + rows[0] * d * channels, out_view_stride=view_stride, out_peer=peer)
 
 
 @dataclass
@@ -397,9 +407,14 @@ class ShardedRender:
             # sort-last composite fused into the render: every rank's kernel stores its row band
             # into rank 0's images over NVLink; the all-reduce after it (stream order) completes it
             out = self._peer_images(n, channels)
+            # rank 0's images are reused by every call: no rank may store this batch's band
+            # before rank 0 has entered the call, i.e. finished with the previous batch
+            # (its host or stream-ordered consumers come before this call)
+            ready = torch.ones(1, dtype=torch.int32, device=self.device)
+            dist.all_reduce(ready, group=self.group)
             if self.r1 > self.r0:
                 self.compute.render_into(local, self.h0, self.shape[0], views, (self.r0, self.r1), channels, fp32,
-                                         out.data_ptr(), d * d * channels)
+                                         out.data_ptr(), d * d * channels, peer=self.rank != 0)
             flag = torch.ones(1, dtype=torch.int32, device=self.device)
             dist.all_reduce(flag, group=self.group)
             return out if self.rank == 0 else None

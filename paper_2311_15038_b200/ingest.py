@@ -22,7 +22,7 @@ import torch
 
 from .device import AtlasSpec
 from .errors import DimensionMismatch, InvalidManifest, MissingSlice, UnsupportedPixelFormat
-from .pipeline import PreviewSession
+from .pipeline import PreviewSession, check_top
 from .types import FACTORY, plan_scheme
 
 
@@ -48,6 +48,19 @@ def read_header(header_path) -> tuple[tuple[int, int, int], Path, object]:
     if size != nx * ny * nz:
         raise DimensionMismatch(f"{raw_path.name}: {size} bytes, header implies {nx * ny * nz}")
     return (nz, ny, nx), raw_path, header.get("voxel_size_um")
+
+
+def _check_session_args(session, shape, n_top: int, frac: float, what: str) -> None:
+    """Before any read: the artifact-bin arguments as artifact_bins checks them
+    (mask.py:223-226), and a reused session must match the volume and arguments."""
+    check_top(n_top, frac, shape[0])
+    if session is None:
+        return
+    if session.shape != shape:
+        raise DimensionMismatch(f"session shape {session.shape} != {what} {shape}")
+    if (session.n_top, session.frac) != (n_top, frac):
+        raise ValueError(f"session built for n_top={session.n_top}, frac={session.frac}; "
+                         f"called with n_top={n_top}, frac={frac}")
 
 
 class RawReader:
@@ -105,6 +118,7 @@ def preview_from_raw(header_path, schemes=(512, 256, 128), n_top: int = 3, frac:
     preadv calls fill each pinned chunk."""
     from .ops import PreviewResult
     shape, raw_path, _ = read_header(header_path)
+    _check_session_args(session, shape, n_top, frac, "volume")
     sch = {}
     for sc in schemes:
         sc = plan_scheme(sc) if isinstance(sc, int) else sc
@@ -112,8 +126,6 @@ def preview_from_raw(header_path, schemes=(512, 256, 128), n_top: int = 3, frac:
     if session is None:
         session = PreviewSession(shape, torch.uint8, {s: AtlasSpec.of(sc) for s, sc in sch.items()}, n_top=n_top,
                                  frac=frac, chunk_slices=chunk_slices)
-    elif session.shape != shape:
-        raise DimensionMismatch(f"session shape {session.shape} != volume {shape}")
     with RawReader(raw_path, shape, threads=threads) as rd:
         out = session.run_reader(rd)
     slicemaps = {}
@@ -145,6 +157,13 @@ def _open_slice(path: Path):
     return im
 
 
+class ManifestPaths(list):
+    """The resolved slice paths, with ``names``: the manifest entries as written
+    (the reference formats its slice-size message with the entry, volume.py:199)."""
+
+    names: list
+
+
 def read_manifest(manifest_path) -> tuple[list, tuple[int, int, int]]:
     """volume.py:176-196: (slice paths in z order, (nz, ny, nx)) or the reference's error."""
     manifest_path = Path(manifest_path)
@@ -159,7 +178,8 @@ def read_manifest(manifest_path) -> tuple[list, tuple[int, int, int]]:
     rel = manifest["slices"]
     if not isinstance(rel, list) or len(rel) == 0:
         raise InvalidManifest(f"{manifest_path}: manifest lists no slices")
-    paths = [manifest_path.parent / name for name in rel]
+    paths = ManifestPaths(manifest_path.parent / name for name in rel)
+    paths.names = [str(name) for name in rel]
     with _open_slice(paths[0]) as im:
         nx, ny = im.size
     return paths, (len(paths), ny, nx)
@@ -173,6 +193,7 @@ class SliceStackReader:
     def __init__(self, paths, shape, threads: int = 8):
         from concurrent.futures import ThreadPoolExecutor
         self.paths = list(paths)
+        self.names = list(getattr(paths, "names", None) or [p.name for p in self.paths])
         self.shape = tuple(shape)
         self._pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
 
@@ -180,7 +201,7 @@ class SliceStackReader:
         path = self.paths[z]
         with _open_slice(path) as im:
             if (im.size[1], im.size[0]) != self.shape[1:]:
-                raise DimensionMismatch(f"slice {path.name}: {im.size} does not match first slice "
+                raise DimensionMismatch(f"slice {self.names[z]}: {im.size} does not match first slice "
                                         f"{(self.shape[2], self.shape[1])}")
             dst[...] = np.asarray(im, dtype=np.uint8)
 
@@ -210,6 +231,7 @@ def preview_from_slice_stack(manifest_path, schemes=(512, 256, 128), n_top: int 
     ``PreviewResult`` (histogram, artifact bins, per-scheme SlicemapSets)."""
     from .ops import PreviewResult
     paths, shape = read_manifest(manifest_path)
+    _check_session_args(session, shape, n_top, frac, "stack")
     sch = {}
     for sc in schemes:
         sc = plan_scheme(sc) if isinstance(sc, int) else sc
@@ -217,8 +239,6 @@ def preview_from_slice_stack(manifest_path, schemes=(512, 256, 128), n_top: int 
     if session is None:
         session = PreviewSession(shape, torch.uint8, {s: AtlasSpec.of(sc) for s, sc in sch.items()}, n_top=n_top,
                                  frac=frac, chunk_slices=chunk_slices)
-    elif session.shape != shape:
-        raise DimensionMismatch(f"session shape {session.shape} != stack {shape}")
     with SliceStackReader(paths, shape, threads=threads) as rd:
         out = session.run_reader(rd)
     slicemaps = {}

@@ -26,6 +26,15 @@ from . import device as dev
 from .device import AtlasSpec
 
 
+def check_top(n_top: int, frac: float, nz: int) -> None:
+    """mask.py:223-226: the artifact-bin arguments, checked before any read or launch."""
+    from .errors import RangeOutOfBounds
+    if not 1 <= n_top <= nz:
+        raise RangeOutOfBounds(f"n_top {n_top} outside [1, {nz}]")
+    if frac < 0:
+        raise RangeOutOfBounds(f"frac {frac} must be non-negative")
+
+
 def level_for_target(shape, target) -> int | None:
     """Return l if target == shape >> l on every axis with exact division (l <= 4)."""
     nz, ny, nx = shape
@@ -140,6 +149,7 @@ class PreviewSession:
                  chunk_slices: int = 64, ring: int = 3, device=None):
         self.shape = tuple(shape)
         self.dtype = dtype
+        check_top(n_top, frac, self.shape[0])
         self.n_top, self.frac = n_top, frac
         self.device = torch.device(device or "cuda")
         self.plan = plan_preview(self.shape, schemes)

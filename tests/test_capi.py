@@ -101,9 +101,9 @@ def test_launch_counter_starts_at_zero(lib):
 def test_validation_errors_without_gpu_newer_entry_points(lib):
     # slab rendering: the slab must lie inside the volume
     view = _lib.View()
-    rc = lib.ctp_render_slab_u8(C.c_void_p(16), 90, 20, 100, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, None)
+    rc = lib.ctp_render_slab_u8(C.c_void_p(16), 90, 20, 100, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, 0, None)
     assert rc == _lib.CTP_E_INVALID and "slab" in _err(lib)
-    rc = lib.ctp_render_slab_u8(None, 0, 8, 8, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, None)
+    rc = lib.ctp_render_slab_u8(None, 0, 8, 8, 8, 8, C.byref(view), 1, 0, 16, C.c_void_p(16), 0, 0, None)
     assert rc == _lib.CTP_E_INVALID
     # PNG filtering and IPC argument checks
     rc = lib.ctp_png_filter_u8(None, 1, 4, 4, -1, C.c_void_p(16), None)

@@ -163,6 +163,24 @@ def _write_stack(tmp, vol, name="stack", manifest=None, mode="L"):
     return tmp / f"{name}.json"
 
 
+def test_ingest_checks_artifact_arguments_before_reading(tmp_path):
+    """n_top outside [1, nz] and a negative frac raise RangeOutOfBounds (mask.py:223-226)
+    before any read or device allocation, in both ingest entry points and PreviewSession."""
+    from paper_2311_15038_b200 import errors as E
+    from paper_2311_15038_b200.ingest import preview_from_raw, preview_from_slice_stack
+    from paper_2311_15038_b200.pipeline import PreviewSession
+    vol = np.random.default_rng(5).integers(0, 256, size=(2, 16, 16), dtype=np.uint8)
+    raw = _write(tmp_path, "two", vol)
+    stack = _write_stack(tmp_path, vol, name="two_stack")
+    for kw in ({"n_top": 3}, {"n_top": 0}, {"frac": -1e-3}):
+        with pytest.raises(E.RangeOutOfBounds):
+            preview_from_raw(raw, schemes=(16,), **kw)
+        with pytest.raises(E.RangeOutOfBounds):
+            preview_from_slice_stack(stack, schemes=(16,), **kw)
+        with pytest.raises(E.RangeOutOfBounds):
+            PreviewSession(vol.shape, None, {}, **kw)
+
+
 def test_slice_stack_manifest_errors_and_reader(tmp_path):
     """read_manifest / SliceStackReader raise load_slice_stack's error classes under
     its conditions and decode the slices in z order."""
@@ -250,12 +268,16 @@ def test_slice_stack_errors_match_load_slice_stack(tmp_path):
     Image.fromarray(np.zeros((8, 9), np.uint8)).save(tmp_path / "odd.png")
     (tmp_path / "mixed.json").write_text(json.dumps({"slices": ["stack_0000.png", "odd.png"]}))
     cases["mixed"] = tmp_path / "mixed.json"
+    (tmp_path / "sub").mkdir()
+    Image.fromarray(np.zeros((8, 9), np.uint8)).save(tmp_path / "sub" / "odd.png")
+    (tmp_path / "mixed_sub.json").write_text(json.dumps({"slices": ["stack_0000.png", "sub/odd.png"]}))
+    cases["mixed_sub"] = tmp_path / "mixed_sub.json"
     code = ("import sys, json; sys.path.insert(0, %r)\n"
             "from ctprev.volume import load_slice_stack\n"
             "out = {}\n"
             "for k, p in json.loads(sys.argv[1]).items():\n"
             "    try:\n        v = load_slice_stack(p); out[k] = int(v.voxels.astype('int64').sum())\n"
-            "    except Exception as e:\n        out[k] = type(e).__name__\n"
+            "    except Exception as e:\n        out[k] = type(e).__name__ + ': ' + str(e)\n"
             "print(json.dumps(out))\n") % str(REF)
     r = subprocess.run([sys.executable, "-c", code, json.dumps({k: str(p) for k, p in cases.items()})],
                        capture_output=True, text=True, env={"NUMBA_CACHE_DIR": "/tmp/numba_cache_ingest",
@@ -270,5 +292,5 @@ def test_slice_stack_errors_match_load_slice_stack(tmp_path):
                 rd(0, shape[0], out)
             got = int(out.astype(np.int64).sum())
         except Exception as e:
-            got = type(e).__name__
-        assert got == ref[k], (k, got, ref[k])
+            got = type(e).__name__ + ": " + str(e)
+        assert got == ref[k], (k, got, ref[k])   # class AND message (volume.py:199 names the manifest entry)

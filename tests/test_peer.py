@@ -4,7 +4,8 @@ slab's cell rows there directly.  Two processes on ONE GPU (gloo for the host
 collectives): the kernels never wait on one another -- each runs to completion
 on its own, the gloo all-reduce orders them -- so this is a functional test of
 the IPC path, not a timing one.  Rank 0's atlases must equal the single-process
-step bit for bit."""
+step bit for bit after EVERY step of a multi-step run on different volumes (the
+peer stores of step k+1 must not overwrite what rank 0 still reads of step k)."""
 from __future__ import annotations
 
 import os
@@ -44,17 +45,26 @@ def _worker(rank, world, port, q):
         fused = {1: schemes[128], 2: schemes[64]}
         sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, fused), rank, world,
                             device, peer_atlases=True)
-        slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)
-        res = sh.step(slab)
-        torch.cuda.synchronize()
-        dist.barrier()
+        # several steps on DIFFERENT volumes, no barrier between them: rank 1 may run ahead
+        # into step k+1 while rank 0 still checks step k's atlases -- the LUT all-reduce must
+        # hold rank 1's stores into rank 0's atlases back until rank 0 has entered step k+1
+        bad = []
+        for k in range(3):
+            spec_k = synth.small((256, 256, 256), seed=3 + k)
+            slab = synth.generate(spec_k, z_range=(sh.z0, sh.z1), device=device)
+            res = sh.step(slab)
+            if rank == 0:
+                torch.cuda.synchronize()
+                got = {l: res["atlases"][l].clone() for l in (1, 2)}
+                got_hist = res["hist"].clone()
+                full = synth.generate(spec_k, device=device)
+                outs, hist, _, _ = dev.preview_step(full, fused, 3, 0.0005)
+                torch.cuda.synchronize()
+                if not (torch.equal(got_hist, hist) and torch.equal(got[1], outs[1]) and torch.equal(got[2], outs[2])):
+                    bad.append(k)
+                del full
         if rank == 0:
-            full = synth.generate(spec, device=device)
-            outs, hist, _, _ = dev.preview_step(full, fused, 3, 0.0005)
-            torch.cuda.synchronize()
-            ok = torch.equal(res["hist"], hist)
-            ok &= torch.equal(res["atlases"][1], outs[1]) and torch.equal(res["atlases"][2], outs[2])
-            q.put(("ok" if ok else "mismatch", (sh.z0, sh.z1)))
+            q.put(("ok" if not bad else f"mismatch at steps {bad}", (sh.z0, sh.z1)))
         dist.barrier()
         sh.close()
         dist.destroy_process_group()
@@ -83,14 +93,20 @@ def _render_worker(rank, world, port, q):
                  for m in ("mip",) for a in (0.0, 70.0, 200.0)]
         sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
         local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
-        out = sr.render(local, views, channels=4, fp32=True)
-        torch.cuda.synchronize()
-        dist.barrier()
+        full = synth.generate(spec, device=device) if rank == 0 else None
+        bad = []
+        for k, az in enumerate((0.0, 35.0, 110.0)):  # batches of different views, no barrier between
+            vk = [ViewParams(azimuth_deg=v.azimuth_deg + az, image_dim=dim, steps=v.steps, mode=v.mode) for v in views]
+            out = sr.render(local, vk, channels=4, fp32=True)
+            if rank == 0:
+                torch.cuda.synchronize()
+                got = out.clone()
+                ref = dev.render(full, vk, channels=4, fp32=True)
+                torch.cuda.synchronize()
+                if not torch.equal(got, ref):
+                    bad.append(k)
         if rank == 0:
-            full = synth.generate(spec, device=device)
-            ref = dev.render(full, views, channels=4, fp32=True)
-            torch.cuda.synchronize()
-            q.put(("ok" if torch.equal(out, ref) else "mismatch", (sr.bands, sr.held)))
+            q.put(("ok" if not bad else f"mismatch at batches {bad}", (sr.bands, sr.held)))
         dist.barrier()
         sr.close()
         dist.destroy_process_group()
