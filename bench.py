@@ -127,126 +127,6 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference: the numpy oracle port of ctprev's algorithm (oracle/ctp_oracle.py),
-# fanned out over z-slabs on all host cores (exact: hist per slab is summed,
-# the filter is per voxel, downscale is block-separable on blocks of whole level-3 cells)
-
-_CPU_VOL = None
-
-
-def _cpu_slab(args):
-    z0, z1, y0, y1, lut = args
-    from oracle import ctp_oracle as O
-    v = _CPU_VOL[z0:z1, y0:y1]
-    h = O.histogram(v)                                   # volume.py:252-262 per block
-    f = O.apply_lut(v, lut)                              # mask.py:246
-    nz, ny, nx = v.shape
-    out = []
-    for s in SCHEMES:                                    # pipeline.py:275: every level direct from f
-        r = _CPU_VOL.shape[2] // s
-        out.append(O.downscale(f, (nx // r, ny // r, nz // r)))
-    return z0, y0, h, out
-
-
-def cpu_reference_pass(vol, z_lo: int, z_hi: int, pool=None, lut=None):
-    """hist + bins (top slab of the FULL volume) + filter + 3 levels + atlas packing of
-    slices [z_lo, z_hi) (z_lo, z_hi multiples of 8: whole level-3 cells; only the
-    atlas maps those slices fall in are packed).  The work is cut into blocks of 8-64
-    slices x a band of rows (multiples of 8: whole level-3 cells) so that every pool
-    worker has work even for a small sample.  Returns voxels processed."""
-    import numpy as np
-    from oracle import ctp_oracle as O
-    if lut is None:  # once per volume (callers timing many small samples pass it in)
-        lut = O.filter_lut(O.artifact_bins(vol))          # mask.py:215-231 (top 3 slices)
-    ny, nx = vol.shape[1], vol.shape[2]
-    workers = getattr(pool, "_processes", 1) if pool else 1
-    nzb = max(1, (z_hi - z_lo) // 64)
-    zstep = max(8, ((z_hi - z_lo) // nzb) // 8 * 8)
-    nyb = max(1, min(ny // 8, -(-2 * workers // max(1, -(-(z_hi - z_lo) // zstep)))))
-    ystep = max(8, (ny // nyb) // 8 * 8)
-    tasks = [(z, min(z + zstep, z_hi), y, min(y + ystep, ny), lut)
-             for z in range(z_lo, z_hi, zstep) for y in range(0, ny, ystep)]
-    results = pool.map(_cpu_slab, tasks) if pool else list(map(_cpu_slab, tasks))
-    hist = np.zeros(256, dtype=np.int64)
-    levels = {s: np.zeros(((z_hi - z_lo) * s // nx, s, s), dtype=np.uint8) for s in SCHEMES}
-    for z0, y0, h, out in results:
-        hist += h
-        for s, lv in zip(SCHEMES, out):
-            r = nx // s
-            levels[s][(z0 - z_lo) // r: (z0 - z_lo) // r + lv.shape[0], y0 // r: y0 // r + lv.shape[1]] = lv
-    for s in SCHEMES:                                    # slicemap.py:132-141 packing
-        sc = O.plan_scheme(s)
-        g = sc[2]
-        per = g * g
-        r = nx // s
-        lz0, lz1 = z_lo // r, z_hi // r
-        for m in range(lz0 // per, -(-lz1 // per)):
-            blk = np.zeros((per, s, s), dtype=np.uint8)
-            a0, a1 = max(m * per, lz0), min((m + 1) * per, lz1)
-            blk[a0 - m * per:a1 - m * per] = levels[s][a0 - lz0:a1 - lz0]
-            _ = blk.reshape(g, g, s, s).transpose(0, 2, 1, 3).reshape(g * s, g * s).copy()
-    return (z_hi - z_lo) * vol.shape[1] * vol.shape[2]
-
-
-def _c2_host_volume():
-    import numpy as np
-    try:
-        import torch
-        from paper_2311_15038_b200 import synth
-        if torch.cuda.is_available():
-            v = synth.generate(synth.config("c2")).cpu().numpy()
-            torch.cuda.empty_cache()
-            return v
-    except Exception:
-        pass
-    rng = np.random.default_rng(0)
-    return np.clip(np.rint(rng.normal(20, 6, (1024, 1024, 1024)).astype(np.float32)), 0, 255).astype(np.uint8)
-
-
-def run_reference(args):
-    """--impl reference: rank 0 only, all host threads, bounded sample per step."""
-    if int(os.environ.get("RANK", "0")) != 0:
-        return 0
-    import multiprocessing as mp
-    global _CPU_VOL
-    workers = os.cpu_count() or 1
-    _CPU_VOL = _c2_host_volume()
-    with mp.get_context("fork").Pool(workers) as pool:
-        from oracle import ctp_oracle as O
-        lut = O.filter_lut(O.artifact_bins(_CPU_VOL))    # per volume (mask.py:215-231): 0.2% of a volume's work
-        cpu_reference_pass(_CPU_VOL, 0, 64, pool, lut)
-        t = time.perf_counter()
-        cpu_reference_pass(_CPU_VOL, 0, 64, pool, lut)
-        per_slice = (time.perf_counter() - t) / 64
-        # size each step so the whole run stays around ~2 minutes (whole level-3 cells: multiples of 8)
-        budget_s = 120.0 / max(1, args.steps + args.warmup)
-        sample = int(max(8, min(1024, budget_s / max(per_slice, 1e-6))) // 8 * 8)
-        for _ in range(args.warmup):
-            cpu_reference_pass(_CPU_VOL, 0, sample, pool, lut)
-        t0 = time.perf_counter()
-        vox = 0
-        for i in range(args.steps):
-            z0 = (i * sample) % 1024
-            z0 = min(z0, 1024 - sample)
-            vox += cpu_reference_pass(_CPU_VOL, z0, z0 + sample, pool, lut)
-        dt = time.perf_counter() - t0
-    v = vox / dt / 1e9
-    line = {"metric": METRIC, "value": v, "unit": "GVoxel/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic (config-2 generator)",
-            "impl": "reference",
-            "config": {"workload": "c2: 1024^3 u8, hist + artifact-bin filter + 512/256/128 levels + atlases",
-                       "sample_slices_per_step": sample},
-            "cpu_baseline": {"value": v, "unit": "GVoxel/s", "cores": workers, "kind": "port",
-                             "sample": f"{sample} of 1024 z-slices per step: hist + filter + levels + atlas packing of "
-                                       "the maps they fall in (artifact bins once per volume); numpy oracle port of "
-                                       "ctprev, process pool over blocks of <= 64 slices x row bands"},
-            "e2e": {"value": v, "unit": "GVoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
-    return 0
-
-
-# ---------------------------------------------------------------------------
 # GPU arm
 
 def main():
@@ -262,7 +142,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the c1 / c3 / c4-alpha side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
-        return run_reference(args)
+        import bench_ref  # numpy + ctprev only: never this package or its .so
+        return bench_ref.run_reference(args)
 
     import torch
     import torch.distributed as dist
@@ -355,49 +236,14 @@ def main():
         except Exception:
             traffic = None
 
-    # ---- e2e through the host-buffer session (pinned host slab in, pinned atlases out)
-    e2e = None
+    # ---- e2e: the reference-facing drop-in calls on a pageable host Volume (the headline
+    # e2e), and the host-buffer session on a pinned volume (side key)
+    e2e = e2e_session = None
     if not args.no_e2e:
-        sess = PreviewSession(spec.shape, torch.uint8, schemes, chunk_slices=64, device=device)
-        host = torch.empty(sess.shape, dtype=torch.uint8, pin_memory=True)
-        host.copy_(slab)
-        for _ in range(2):
-            sess.run(host)
-        e_steps = 10
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        w0 = time.perf_counter()
-        for _ in range(e_steps):
-            sess.run(host)
-        torch.cuda.synchronize()
-        e_s = time.perf_counter() - w0
-        et = torch.tensor([e_s], dtype=torch.float64, device=device)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_s = float(et.item())
-        vox_e2e = sess.shape[0] * ny * nx * (world if world > 1 else 1)
-        # the PCIe bound of this path: a plain pinned H2D copy of the same 1 GiB
-        h2d = torch.empty(sess.shape, dtype=torch.uint8, device=device)
-        h2d.copy_(host, non_blocking=True)
-        torch.cuda.synchronize()
-        c0 = torch.cuda.Event(enable_timing=True)
-        c1 = torch.cuda.Event(enable_timing=True)
-        c0.record()
-        for _ in range(3):
-            h2d.copy_(host, non_blocking=True)
-        c1.record()
-        torch.cuda.synchronize()
-        h2d_gbs = 3 * host.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9
-        del h2d
-        e_gbs = sess.h2d_bytes * e_steps / e_s / 1e9
-        e2e = {"value": vox_e2e * e_steps / e_s / 1e9, "unit": "GVoxel/s",
-               "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes, "steps": e_steps,
-               "h2d_GBps": e_gbs, "pcie_h2d_copy_GBps": h2d_gbs, "pcie_frac": e_gbs / h2d_gbs,
-               "path": "PreviewSession.run(pinned host volume): z-chunk streamed H2D / fused pass / atlas D2H on "
-                       "3 CUDA streams" + ("" if world == 1 else "; one scan per rank")}
-        del sess, host
-        torch.cuda.empty_cache()
+        host_np = slab.cpu().numpy()
+        e2e = bench_e2e_dropin(host_np, device, world, dist)
+        e2e_session = bench_e2e_session(slab, spec, schemes, device, world, dist)
+        del host_np
 
     # ---- N > 1: ONE c2 volume z-slab sharded across the ranks (strong scaling): LUT broadcast
     # from the top-slab owner, fused pass per slab storing its atlas rows into rank 0's atlases
@@ -434,23 +280,12 @@ def main():
         torch.cuda.empty_cache()
         slab = synth.generate(synth.config("c2", seed=rank), device=device)
 
-    # ---- CPU baseline (rank 0, N=1 only): the oracle port on all host cores, bounded sample
+    # ---- CPU baseline (rank 0, N=1 only): ctprev's own functions (baseline/_ref; the oracle
+    # port when absent) fanned out over all host cores on 512 slices of this volume
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import multiprocessing as mp
-        global _CPU_VOL
-        _CPU_VOL = slab.cpu().numpy()
-        workers = os.cpu_count() or 1
-        with mp.get_context("fork").Pool(workers) as pool:
-            cpu_reference_pass(_CPU_VOL, 0, 64, pool)
-            c0 = time.perf_counter()
-            n = cpu_reference_pass(_CPU_VOL, 0, 512, pool)
-            c_s = time.perf_counter() - c0
-        cpu = {"value": n / c_s / 1e9, "unit": "GVoxel/s", "cores": workers, "kind": "port",
-               "sample": "512 of 1024 z-slices of the same c2 volume: hist + artifact bins + filter + 512/256/128 "
-                         "levels + atlas packing (numpy oracle port of ctprev, process pool over blocks of slices x row bands)",
-               "seconds": c_s}
-        _CPU_VOL = None
+        import bench_ref
+        cpu = bench_ref.cpu_baseline(slab.cpu().numpy(), 512)
 
     mip = None
     if not args.no_mip:
@@ -481,6 +316,7 @@ def main():
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_session": e2e_session,
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "mip": mip,
@@ -491,6 +327,126 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_e2e_dropin(vol_np, device, world, dist, steps: int = 8, warmup: int = 2):
+    """e2e through the reference-facing API: ctprev's OWN entry points with ``install()``
+    (ctprev from baseline/_ref; this package's drop-ins directly when it is absent), the
+    config-2 composition of SURVEY s8(d) on a pageable host Volume:
+        volume_histogram(v); bins = artifact_bins(v); f = filter_histogram_bins(v, bins)
+        L_s = downscale_volume(f, (s, s, s)); encode_slicemaps(L_s, s)   for s = 512, 256, 128
+    Every call returns fresh host arrays (the reference's contract).  The device cache is
+    cleared at the start of every step, so each step uploads its volume (1 GiB H2D) and
+    reads back the filtered volume, the levels and the atlases; within a step the chain
+    runs from HBM (f and the levels are not re-uploaded)."""
+    import torch
+    from paper_2311_15038_b200 import _lib, hostio, ops
+    api, how = ops, "paper_2311_15038_b200 drop-ins (ctprev not importable)"
+    uninstall = None
+    try:
+        ref_dir = ROOT / "baseline" / "_ref"
+        if ref_dir.is_dir() and str(ref_dir) not in sys.path:
+            sys.path.insert(0, str(ref_dir))
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ctp_ref_numba_cache")
+        import ctprev
+        from paper_2311_15038_b200.install import install, uninstall
+        install()
+        api, how = ctprev, f"ctprev's own namespace after install() ({Path(ctprev.__file__).parent})"
+    except Exception:  # pragma: no cover - depends on the box
+        pass
+    try:
+        from paper_2311_15038_b200.types import FACTORY
+        v = FACTORY.Volume(vol_np)
+        nz, ny, nx = vol_np.shape
+        sizes = {}
+
+        def step():
+            hostio.CACHE.clear()
+            h = api.volume_histogram(v)                                   # volume.py:252-262
+            bins = api.artifact_bins(v)                                   # mask.py:215-231
+            f = api.filter_histogram_bins(v, bins)                        # mask.py:234-246
+            out = [h.bins.nbytes, f.voxels.nbytes]
+            for s in SCHEMES:
+                lv = api.downscale_volume(f, (s, s, s))                   # volume.py:277-309
+                sm = api.encode_slicemaps(lv, s)                          # slicemap.py:120-142
+                out += [lv.voxels.nbytes, sum(a.nbytes for a in sm.atlases)]
+            sizes["d2h"] = sum(out)
+            return h
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches0 = _lib.launch_count()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            h = step()
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+        launches = _lib.launch_count() - launches0
+        st = torch.tensor([sec], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        sec = float(st.item())
+        assert int(h.bins.sum()) == nz * ny * nx
+        hostio.CACHE.clear()
+        return {"value": world * nz * ny * nx * steps / sec / 1e9, "unit": "GVoxel/s",
+                "h2d_bytes_per_step": nz * ny * nx + 3 * ny * nx + 256, "d2h_bytes_per_step": sizes["d2h"],
+                "steps": steps, "ms_per_step": sec / steps * 1e3, "gpu_launches_per_step": launches / steps,
+                "path": how + ": volume_histogram, artifact_bins, filter_histogram_bins, downscale_volume x3, "
+                        "encode_slicemaps x3 on a pageable 1 GiB Volume; fresh host arrays out; device cache "
+                        "cleared every step" + ("" if world == 1 else f"; one volume per rank x{world}")}
+    finally:
+        if uninstall is not None:
+            uninstall()
+
+
+def bench_e2e_session(slab, spec, schemes, device, world, dist):
+    """Side key: the host-buffer session (pinned volume in, pinned atlases out, z-chunks
+    streamed on three CUDA streams) -- this package's own streaming API."""
+    import torch
+    from paper_2311_15038_b200.pipeline import PreviewSession
+    nz, ny, nx = spec.shape
+    sess = PreviewSession(spec.shape, torch.uint8, schemes, chunk_slices=64, device=device)
+    host = torch.empty(sess.shape, dtype=torch.uint8, pin_memory=True)
+    host.copy_(slab)
+    for _ in range(2):
+        sess.run(host)
+    e_steps = 10
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    w0 = time.perf_counter()
+    for _ in range(e_steps):
+        sess.run(host)
+    torch.cuda.synchronize()
+    e_s = time.perf_counter() - w0
+    et = torch.tensor([e_s], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e_s = float(et.item())
+    # the PCIe bound of this path: a plain pinned H2D copy of the same 1 GiB
+    h2d = torch.empty(sess.shape, dtype=torch.uint8, device=device)
+    h2d.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(3):
+        h2d.copy_(host, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * host.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    e_gbs = sess.h2d_bytes * e_steps / e_s / 1e9
+    out = {"value": world * nz * ny * nx * e_steps / e_s / 1e9, "unit": "GVoxel/s",
+           "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes, "steps": e_steps,
+           "h2d_GBps": e_gbs, "pcie_h2d_copy_GBps": h2d_gbs, "pcie_frac": e_gbs / h2d_gbs,
+           "path": "PreviewSession.run(pinned host volume): z-chunk streamed H2D / fused pass / atlas D2H on "
+                   "3 CUDA streams" + ("" if world == 1 else f"; one volume per rank x{world}")}
+    del sess, host, h2d
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_mip(args, device, rank, world, dist, sort_last: bool = False):

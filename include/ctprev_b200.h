@@ -297,13 +297,15 @@ typedef struct ctp_shell {
 } ctp_shell;
 
 /* Fill a (z-slab of a) volume: background N(bg_mean, bg_sd) clipped, shells,
- * speckle with probability speckle_p (uniform in [0, vmax]); counter-based
- * hash RNG keyed by (seed, global voxel index), so any slab of the same
- * volume is reproducible.  elem_bytes = 1 (uint8, vmax 255) or 2 (uint16, vmax). */
+ * speckle with probability speckle_p -- uniform in [0, vmax] (speckle_lambda
+ * = 0, config 2) or a Poisson-like count of mean speckle_lambda (the normal
+ * approximation N(lambda, lambda), config 3/5); counter-based hash RNG keyed
+ * by (seed, global voxel index), so any slab of the same volume is
+ * reproducible.  elem_bytes = 1 (uint8, vmax 255) or 2 (uint16, vmax). */
 int ctp_synth_volume(void* vol, int32_t elem_bytes, int64_t nz, int64_t ny, int64_t nx,
                      int64_t z_base, int64_t full_nz, uint64_t seed, float bg_mean, float bg_sd,
                      int32_t vmax, const ctp_shell* shells, int32_t n_shells,
-                     float speckle_p, void* stream);
+                     float speckle_p, float speckle_lambda, void* stream);
 
 /* ---------------- misc --------------------------------------------------- */
 

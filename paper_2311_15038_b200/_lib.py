@@ -102,7 +102,7 @@ SIGNATURES = {
     "ctp_ipc_close": [_P, _I64],
     "ctp_image_hist_u8": [_P, _I32, _I64, _P, _P],
     "ctp_synth_volume": [_P, _I32, _I64, _I64, _I64, _I64, _I64, C.c_uint64, C.c_float, C.c_float, _I32,
-                         C.POINTER(Shell), _I32, C.c_float, _P],
+                         C.POINTER(Shell), _I32, C.c_float, C.c_float, _P],
     "ctp_last_error": [],
     "ctp_abi_version": [],
     "ctp_launch_count": [_I32],

@@ -27,7 +27,7 @@ struct SynthArgs {
   int elem;
   int64_t nz, ny, nx, z_base;
   uint64_t seed;
-  float bg_mean, bg_sd, speckle_p;
+  float bg_mean, bg_sd, speckle_p, speckle_lambda;
   int vmax;
   const ctp_shell* shells;
   int n_shells;
@@ -59,7 +59,12 @@ __global__ void synth_kernel(const SynthArgs a) {
       v = S.mean + S.sd * gauss(splitmix64(h0 ^ (0xD1B54A32D192ED03ull * (uint64_t)(s + 1))));
     }
     const uint64_t h2 = splitmix64(h0 ^ 0xA0761D6478BD642Full);
-    if (u01((uint32_t)h2) < a.speckle_p) v = u01((uint32_t)(h2 >> 32)) * (float)(a.vmax + 1) - 0.5f;
+    if (u01((uint32_t)h2) < a.speckle_p) {
+      if (a.speckle_lambda > 0.0f)  // Poisson-like count: N(lambda, lambda)
+        v = a.speckle_lambda + sqrtf(a.speckle_lambda) * gauss(splitmix64(h2));
+      else
+        v = u01((uint32_t)(h2 >> 32)) * (float)(a.vmax + 1) - 0.5f;
+    }
     float c = rintf(v);
     c = fminf(fmaxf(c, 0.0f), (float)a.vmax);
     if (a.elem == 1) reinterpret_cast<uint8_t*>(a.vol)[o] = (uint8_t)c;
@@ -73,7 +78,8 @@ using namespace ctp;
 
 extern "C" int ctp_synth_volume(void* vol, int32_t elem_bytes, int64_t nz, int64_t ny, int64_t nx, int64_t z_base,
                                 int64_t full_nz, uint64_t seed, float bg_mean, float bg_sd, int32_t vmax,
-                                const ctp_shell* shells, int32_t n_shells, float speckle_p, void* stream) {
+                                const ctp_shell* shells, int32_t n_shells, float speckle_p, float speckle_lambda,
+                                void* stream) {
   CTP_REQUIRE(vol != nullptr, CTP_E_INVALID, "ctp_synth_volume: null volume");
   CTP_REQUIRE(elem_bytes == 1 || elem_bytes == 2, CTP_E_UNSUPPORTED, "elem_bytes must be 1 or 2");
   CTP_REQUIRE(nz >= 1 && ny >= 1 && nx >= 1 && z_base >= 0 && z_base + nz <= full_nz, CTP_E_INVALID,
@@ -86,7 +92,8 @@ extern "C" int ctp_synth_volume(void* vol, int32_t elem_bytes, int64_t nz, int64
     CTP_CUDA_CALL(cudaMallocAsync(reinterpret_cast<void**>(&dsh), sizeof(ctp_shell) * n_shells, st));
     CTP_CUDA_CALL(cudaMemcpyAsync(dsh, shells, sizeof(ctp_shell) * n_shells, cudaMemcpyHostToDevice, st));
   }
-  SynthArgs a{vol, elem_bytes, nz, ny, nx, z_base, seed, bg_mean, bg_sd, speckle_p, vmax, dsh, n_shells};
+  CTP_REQUIRE(speckle_lambda >= 0.0f, CTP_E_INVALID, "speckle_lambda must be >= 0");
+  SynthArgs a{vol, elem_bytes, nz, ny, nx, z_base, seed, bg_mean, bg_sd, speckle_p, speckle_lambda, vmax, dsh, n_shells};
   synth_kernel<<<num_sms() * 8, 256, 0, st>>>(a);
   cudaError_t le = cudaGetLastError();
   if (dsh) cudaFreeAsync(dsh, st);

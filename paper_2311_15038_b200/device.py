@@ -331,7 +331,7 @@ def image_hist(imgs: torch.Tensor) -> torch.Tensor:
 
 def synth(shape, dtype, seed: int, bg_mean: float, bg_sd: float, shells, speckle_p: float,
           vmax: int | None = None, z_base: int = 0, full_nz: int | None = None, device=None,
-          out: torch.Tensor | None = None) -> torch.Tensor:
+          out: torch.Tensor | None = None, speckle_lambda: float = 0.0) -> torch.Tensor:
     nz, ny, nx = shape
     full_nz = full_nz if full_nz is not None else z_base + nz
     elem = 1 if dtype == torch.uint8 else 2
@@ -342,7 +342,7 @@ def synth(shape, dtype, seed: int, bg_mean: float, bg_sd: float, shells, speckle
     for i, s in enumerate(shells):
         arr[i] = _lib.Shell(*[float(x) for x in s], 0.0)
     _lib.call("ctp_synth_volume", _ptr(out), elem, nz, ny, nx, z_base, full_nz, seed, bg_mean, bg_sd, vmax,
-              arr, len(shells), speckle_p, _stream())
+              arr, len(shells), speckle_p, speckle_lambda, _stream())
     return out
 
 

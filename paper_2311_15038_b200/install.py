@@ -37,9 +37,11 @@ BINDINGS = {
 _saved: dict = {}
 
 
-def install(package: str = "ctprev") -> list[str]:
+def install(package: str = "ctprev", exclude=()) -> list[str]:
     """Rebind the reference's hot-path functions to the B200 implementation.
-    Returns the list of patched 'module.name' sites."""
+    Returns the list of patched 'module.name' sites.  ``exclude``: names to leave
+    bound to the reference (e.g. ``("save_slicemaps",)`` keeps Pillow's PNG writer,
+    whose bytes the reference's recorded bundle checksums pin)."""
     root = importlib.import_module(package)
     vol = importlib.import_module(f"{package}.volume")
     sm = importlib.import_module(f"{package}.slicemap")
@@ -57,6 +59,8 @@ def install(package: str = "ctprev") -> list[str]:
     FACTORY.Circle = importlib.import_module(f"{package}.mask").Circle
     patched = []
     for name, mods in BINDINGS.items():
+        if name in exclude:
+            continue
         new = getattr(ops, name)
         for m in mods:
             modname = f"{package}.{m}" if m else package

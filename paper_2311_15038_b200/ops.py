@@ -20,7 +20,6 @@ plus the fused ``preview_pipeline`` (one HBM pass for hist + filter + levels
 """
 from __future__ import annotations
 
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -28,6 +27,7 @@ import torch
 
 from . import _lib
 from . import device as dev
+from . import hostio
 from .device import AtlasSpec
 from .errors import InvalidTarget, RangeOutOfBounds, UnsupportedPixelFormat, DimensionMismatch
 from .pipeline import plan_preview, run_preview
@@ -48,17 +48,24 @@ def cuda_device() -> torch.device:
 
 
 def to_device(arr: np.ndarray) -> torch.Tensor:
-    """H2D of a host array (read-only numpy arrays are fine: the copy never writes)."""
+    """The device copy of a host array: from the device cache when this frozen array
+    was uploaded or produced before (``hostio.DeviceCache``), else a staged H2D copy
+    (cached if the array is frozen).  The result is never written by the callers."""
     dev_ = cuda_device()
-    a = np.ascontiguousarray(arr)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore", UserWarning)  # non-writable numpy -> torch view
-        t = torch.from_numpy(a)
-    return t.to(dev_, non_blocking=False)
+    t = hostio.CACHE.get(arr, dev_)
+    if t is None:
+        t = hostio.h2d(arr, dev_)
+        hostio.CACHE.put(arr, t)
+    return t
 
 
 def _host(t: torch.Tensor) -> np.ndarray:
-    return t.cpu().numpy()
+    return hostio.d2h(t)
+
+
+def _host_volume(t: torch.Tensor) -> np.ndarray:
+    """Voxels of a result Volume: frozen (as Volume would, volume.py:60-62), device copy kept."""
+    return hostio.d2h_frozen(t)
 
 
 def _voxels(volume) -> np.ndarray:
@@ -121,7 +128,7 @@ def filter_histogram_bins(volume, bins):
     lut = _lut_from_bins(bins)
     vox = _voxels(volume)
     out = dev.lut_apply_u8(to_device(vox), to_device(lut))
-    return FACTORY.Volume(_host(out), getattr(volume, "voxel_size_um", None))
+    return FACTORY.Volume(_host_volume(out), getattr(volume, "voxel_size_um", None))
 
 
 # ---------------------------------------------------------------------------
@@ -144,7 +151,7 @@ def downscale_volume(volume, target):
     vs = getattr(volume, "voxel_size_um", None)
     if (tx, ty, tz) == (nx, ny, nz):
         return FACTORY.Volume(vox, vs)
-    return FACTORY.Volume(_host(_downscale_dev(to_device(vox), (tx, ty, tz))), vs)
+    return FACTORY.Volume(_host_volume(_downscale_dev(to_device(vox), (tx, ty, tz))), vs)
 
 
 def _downscale_dev(t: torch.Tensor, target) -> torch.Tensor:
@@ -155,6 +162,32 @@ def _downscale_dev(t: torch.Tensor, target) -> torch.Tensor:
     if l is not None and l >= 1:
         return dev.preview(t, None, {l: "xyz"})[l]
     return dev.downscale(t, target)
+
+
+def _scheme_levels(t: torch.Tensor, sizes) -> dict:
+    """``_scheme_volume(v, s)`` (pipeline.py:215-223) for several schemes at once: every
+    level that is a power-of-two ratio of the volume comes out of ONE fused pass (dense,
+    each straight from full resolution: exact block sums, volume.py:306-308 rounding);
+    identity targets are the volume itself; any other ratio takes the general kernel."""
+    from .pipeline import level_for_target
+    nz, ny, nx = t.shape
+    targets = {s: (min(s, nx), min(s, ny), min(s, nz)) for s in sizes}
+    out, fused = {}, {}
+    for s, tg in targets.items():
+        if tg == (nx, ny, nz):
+            out[s] = t
+        elif nx % 16 == 0:
+            l = level_for_target((nz, ny, nx), tg)
+            if l is not None and l >= 1:
+                fused[s] = l
+    if fused:
+        res = dev.preview(t, None, {l: "xyz" for l in set(fused.values())})
+        for s, l in fused.items():
+            out[s] = res[l]
+    for s, tg in targets.items():
+        if s not in out:
+            out[s] = _downscale_dev(t, tg)
+    return out
 
 
 def encode_slicemaps(volume, scheme):
@@ -177,7 +210,7 @@ def decode_slicemaps(sset):
     sc = sset.scheme
     spec = AtlasSpec.of(sc)
     atl = to_device(np.stack([np.asarray(a) for a in sset.atlases]))
-    return FACTORY.Volume(_host(dev.decode_atlas(atl, spec)))
+    return FACTORY.Volume(_host_volume(dev.decode_atlas(atl, spec)))
 
 
 # ---------------------------------------------------------------------------
@@ -288,9 +321,9 @@ def preview_pipeline(volume, schemes=(512, 256, 128), n_top: int = 3, frac: floa
     for s, sc in sch.items():
         a = _host(res.atlases[s])
         slicemaps[s] = FACTORY.SlicemapSet(scheme=sc, atlases=tuple(a[m] for m in range(sc.map_count)))
-    levels = {s: FACTORY.Volume(_host(t)) for s, t in res.levels.items()}
+    levels = {s: FACTORY.Volume(_host_volume(t)) for s, t in res.levels.items()}
     flags = _host(res.flags)
-    filtered = FACTORY.Volume(_host(res.filtered)) if (keep_filtered and res.filtered is not None) else None
+    filtered = FACTORY.Volume(_host_volume(res.filtered)) if (keep_filtered and res.filtered is not None) else None
     return PreviewResult(_host(res.hist), frozenset(int(b) for b in np.nonzero(flags)[0]), slicemaps, levels,
                          filtered)
 
@@ -339,7 +372,7 @@ def apply_circle_mask(volume, circle, margin: float = 0.02):
         raise RangeOutOfBounds(f"margin {margin} outside [0, 1)")
     r_eff = circle.r * (1.0 - margin)                                        # mask.py:208
     out = dev.circle_mask(to_device(vox), circle.cx, circle.cy, r_eff ** 2)
-    return FACTORY.Volume(_host(out), getattr(volume, "voxel_size_um", None))
+    return FACTORY.Volume(_host_volume(out), getattr(volume, "voxel_size_um", None))
 
 
 def _host_helper(module: str, name: str):
@@ -418,12 +451,8 @@ def build_interactive_preview(volume, detect=None, threshold=None, margin: float
     detect = detect or _host_helper("mask", "detect_container_circle")
     threshold = threshold or _host_helper("threshold", "otsu_threshold")
     vox = _voxels(volume)
-    nz, ny, nx = vox.shape
     t = to_device(vox)
-    downs = {}
-    for s in INTERACTIVE_SCHEMES:
-        target = (min(s, nx), min(s, ny), min(s, nz))                            # pipeline.py:221-222
-        downs[s] = t if target == (nx, ny, nz) else _downscale_dev(t, target)
+    downs = _scheme_levels(t, INTERACTIVE_SCHEMES)                               # pipeline.py:215-223, 286
     warnings_: list[str] = []
     circle = None
     try:

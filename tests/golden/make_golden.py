@@ -323,7 +323,25 @@ def bundle_golden() -> None:
     print(f"wrote {out} ({out.stat().st_size / 1e6:.2f} MB)")
 
 
+def bundle_checksums() -> None:
+    """The mounted meta.json checksums of the two recorded bundles (27 files each),
+    copied to tests/golden/ref_bundle_checksums.json so the GPU box -- which has no
+    /root/reference -- can check a build_bundle run under install() against them."""
+    import json
+    ref = Path("/root/reference/pkg")
+    src = {"fixture-128": ref / "frontend/tests/fixtures/bundles/fixture-128/meta.json",
+           "demo-scan-01": ref / "demos/out/full_pipeline/bundles/demo-scan-01/meta.json"}
+    out = {bid: {"source": str(p.relative_to(ref)), "checksums": json.loads(p.read_text())["checksums"]}
+           for bid, p in src.items()}
+    dst = Path(__file__).resolve().parent / "ref_bundle_checksums.json"
+    dst.write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
+    print(f"wrote {dst}")
+
+
 if __name__ == "__main__":
+    if "--only-checksums" in sys.argv:
+        bundle_checksums()
+        sys.exit(0)
     if "--only-bundles" in sys.argv:
         bundle_golden()
         sys.exit(0)
@@ -335,3 +353,4 @@ if __name__ == "__main__":
     data_preview_golden()
     interactive_preview_golden()
     bundle_golden()
+    bundle_checksums()

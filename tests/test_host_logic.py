@@ -148,3 +148,25 @@ def test_install_rebinds_every_site(monkeypatch, tmp_path):
         inst.uninstall()
     import ctprev.volume
     assert ctprev.volume.volume_histogram is not P.volume_histogram
+
+
+def test_reference_arm_is_independent_of_the_package():
+    """bench_ref (the --impl reference arm) imports numpy + ctprev only: importing it and
+    generating a slab must not import paper_2311_15038_b200 (nor load its .so), and its
+    generator parameters are the GPU arm's synth.config c2 / c4."""
+    import subprocess
+    code = ("import sys; sys.path.insert(0, %r); import bench_ref, numpy as np\n"
+            "out = np.empty((2, 64, 64), np.uint8); p = dict(bench_ref.GEN['c2'], shape=(8, 64, 64))\n"
+            "bench_ref.gen_slab(p, 0, 2, out); bench_ref.headline_config(1)\n"
+            "assert not any(m.startswith('paper_2311_15038_b200') for m in sys.modules), 'package imported'\n"
+            "print('ok', int(out.max()))\n") % str(ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr
+    import bench_ref
+    from paper_2311_15038_b200 import synth
+    for name in ("c2", "c4"):
+        sp, p = synth.config(name), bench_ref.GEN[name]
+        assert (sp.shape, sp.seed, sp.n_shells, (sp.bg_mean, sp.bg_sd), (sp.shell_mean, sp.shell_sd), sp.axes,
+                sp.thickness, sp.speckle_p) == (p["shape"], p["seed"], p["n_shells"], p["bg"], p["shell"], p["axes"],
+                                                p["thickness"], p["speckle_p"]), name
+        assert [tuple(s) for s in sp.shells()] == [tuple(s) for s in bench_ref.shells(p)], name
