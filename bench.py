@@ -627,18 +627,39 @@ def bench_other_configs(device):
         spec = synth.config("c5", seed=0)
         vol = synth.generate(spec, device=device)
         ps = PreviewStream(spec.shape, torch.uint16, device=device)
-        ms = _time_steps(lambda: ps.process(vol), 4, warmup=1)
+        for _ in range(3):
+            ps.process(vol)
+        reps = []
+        for _ in range(10):  # per-volume times with a phase breakdown (CUDA events between phases)
+            ps.trace = []
+            ps.process(vol)
+            torch.cuda.synchronize()
+            tr = ps.trace
+            reps.append({name: a.elapsed_time(b) for (_, a), (name, b) in zip(tr, tr[1:])})
+        ps.trace = None
+        tot = sorted(sum(r.values()) for r in reps)
+        ms = statistics.median(tot)
         n = vol.numel()
-        out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume: hist + filter o rescale + L1..L4 padded "
-                                 "atlases + 36-view 512^2 MIP strip (from L2), one volume per GPU",
-                     "ms_per_volume": ms, "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6}
+        alg = n * 2 + ps.product_bytes - ps.thumbs.numel()
+        out["c5"] = {"workload": "1536^2 x 2048 12-bit u16 (9 GiB) per volume (SURVEY s8(d)): hist + filter o rescale "
+                                 "+ L1..L4 (one fused pass) + _scheme_volume/_pad_to_cube atlases (L1 768^2x1024 -> 512^3 "
+                                 "general downscale; L2..L4 identity + pad into 512/256/128) + 36-view 512^2 MIP strip "
+                                 "(from L2), one volume per GPU",
+                     "ms_per_volume": ms, "ms_min": tot[0], "ms_max": tot[-1], "reps": len(tot),
+                     "phases_ms_median": {k: statistics.median(r[k] for r in reps) for k in reps[0]},
+                     "volumes_per_min_per_gpu": 60000.0 / ms, "gvoxel_per_s": n / ms / 1e6,
+                     "fused_pass_GBps": (n * 2 + sum(ps.levels[l].map_count * ps.levels[l].atlas_dim ** 2
+                                                     for l in ps.levels if l not in ps.dense)
+                                         + sum(t.numel() for t in ps.dense_bufs.values()))
+                                        / (statistics.median(r["fused_pass"] for r in reps) * 1e-3) / 1e9,
+                     "alg_bytes_excl_mip": alg}
         # end to end: volumes from pinned host memory (H2D of volume i+1 on a copy stream while volume i is
         # reduced; two device buffers), every product read back (atlases + thumbnails, D2H), 4 volumes
         try:
             host = torch.empty(spec.shape, dtype=torch.uint16, pin_memory=True)
             host.copy_(vol)
             bufs = [vol, torch.empty_like(vol)]
-            prod = sum(t.numel() for t in ps.atlases.values()) + ps.thumbs.numel()
+            prod = ps.product_bytes
             host_out = torch.empty(prod, dtype=torch.uint8, pin_memory=True)
             cs = torch.cuda.Stream()
             main = torch.cuda.current_stream()

@@ -117,20 +117,32 @@ class PreviewStream:
         self.views = [ViewParams(azimuth_deg=360.0 * k / n_views, image_dim=thumb_dim, steps=self.steps, mode="mip")
                       for k in range(n_views)]
         self.thumbs = torch.empty((n_views, thumb_dim, thumb_dim, 4), dtype=torch.uint8, device=self.device)
+        self.trace = None  # a list -> process() appends (phase, CUDA event) after each phase (bench breakdown)
+
+    def _mark(self, name: str) -> None:
+        if self.trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.trace.append((name, e))
 
     @property
     def product_bytes(self) -> int:
         return sum(sp.map_count * sp.atlas_dim ** 2 for sp in self.levels.values()) + self.thumbs.numel()
 
     def process(self, vol: torch.Tensor) -> StreamResult:
+        self._mark("start")
         outputs = {l: ("xyz" if l in self.dense else sp) for l, sp in self.levels.items()}
         tensors = {l: (self.dense_bufs[l] if l in self.dense else self.atlases[l]) for l in self.levels}
         _, _, lut, flags = dev.preview_step(vol, outputs, 3, 0.0005, hist=self.hist, out_tensors=tensors)
+        self._mark("fused_pass")
         for l in sorted(self.dense):
             lz, ly, lx = self.level_shape[l]
             src = self.dense_bufs[l]
             if self.targets[l] != (lx, ly, lz):  # _scheme_volume: the general-ratio box mean (volume.py:277-309)
                 src = dev.downscale(src, self.targets[l])
+                self._mark(f"downscale_L{l}")
             self.atlases[l] = dev.encode_atlas(src, self.levels[l])     # pack + _pad_to_cube (pipeline.py:226-237)
+            self._mark(f"encode_L{l}")
         dev.render(self.dense_bufs[self.thumb_level], self.views, channels=4, fp32=True, out=self.thumbs)
+        self._mark("mip_strip")
         return StreamResult(self.hist, flags, self.atlases, self.thumbs)

@@ -387,52 +387,74 @@ def test_batched_views_equal_single_views(P, golden):
 
 # ---------------------------------------------------------------- config 3 at full size (16 GiB)
 
-def test_preview_c3_full_size_spot_checks(P, cuda):
-    """Config 3 exactly (2048^3 12-bit u16, 20 shells, speckle): the 4096-bin
-    histogram is checked against per-slab oracle bincounts (exact, chunked), the
-    artifact LUT against the oracle on the top slab, and every level's atlas at
-    2000 random cells against the block mean recomputed from the source voxels
-    (a size-independent property: the oracle never holds the 16 GiB volume)."""
+# Full-size configs 3 and 5 are checked against the oracle on EVERY atlas byte:
+# the source is copied to the host once and the oracle runs chunk by chunk on a
+# fork pool (levels are separable on slabs of whole 2^L cells, volume.py:265-309;
+# histograms of slabs sum), so it never needs the whole filtered volume at once.
+_SRC = None   # host copy of the source volume, inherited by the forked workers
+_LUT = None
+
+
+def _chunk_levels(args):
+    z0, z1, nlev = args
+    v = _SRC[z0:z1]
+    h = O.histogram_u16(v)
+    f = _LUT[np.minimum(v, 4095)]                                   # filter o rescale (DESIGN s4)
+    cz, ny, nx = f.shape
+    return z0, h, [O.downscale(f, (nx >> l, ny >> l, cz >> l)) for l in range(1, nlev + 1)]  # volume.py:277-309
+
+
+def _chunked_oracle(vol_t, nlev: int, chunk: int = 16):
+    """(hist, bins, lut, {l: level}) of a 12-bit volume, every level direct from the
+    filtered full-resolution voxels (pipeline.py:275), computed in z-chunks."""
+    import multiprocessing as mp
+    import os
+    global _SRC, _LUT
+    _SRC = vol_t.cpu().numpy()
+    nz, ny, nx = _SRC.shape
+    bins = O.artifact_bins_u16(_SRC[nz - 3:])                      # mask.py:215-231 over 4096 bins
+    _LUT = O.lut_u16(bins)
+    levels = {l: np.empty((nz >> l, ny >> l, nx >> l), np.uint8) for l in range(1, nlev + 1)}
+    hist = np.zeros(4096, np.int64)
+    try:
+        with mp.get_context("fork").Pool(os.cpu_count() or 4) as pool:
+            for z0, h, lv in pool.imap_unordered(_chunk_levels, [(z, z + chunk, nlev) for z in range(0, nz, chunk)]):
+                hist += h
+                for l, a in zip(range(1, nlev + 1), lv):
+                    levels[l][z0 >> l:(z0 >> l) + a.shape[0]] = a
+    finally:
+        _SRC = None
+    return hist, bins, _LUT, levels
+
+
+def test_preview_c3_full_size_every_atlas_byte(P, cuda):
+    """Config 3 exactly (2048^3 12-bit u16, 16 GiB): 4096-bin histogram, artifact LUT
+    and EVERY byte of all four levels' atlases (1024: 64 maps of 4x4 4096^2; planned
+    512/256/128) against the chunked oracle."""
     import torch
-    from paper_2311_15038_b200 import device as dev, synth
+    from paper_2311_15038_b200 import synth
     from paper_2311_15038_b200.device import AtlasSpec
     from paper_2311_15038_b200.pipeline import plan_preview, run_preview
 
     spec = synth.config("c3")
     vol = synth.generate(spec, device=cuda)
-    nz, ny, nx = spec.shape
     schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec(512, 4096, 8, 8),
                256: AtlasSpec(256, 2048, 8, 4), 128: AtlasSpec(128, 1024, 8, 2)}
     plan = plan_preview(spec.shape, schemes)
     assert not plan.general and plan.nlev == 4
     res = run_preview(vol, plan)
-    hist = res.hist.cpu().numpy()
-    # exact histogram, 128-slice slabs on the host
-    want = np.zeros(4096, dtype=np.int64)
-    for z in range(0, nz, 128):
-        want += O.histogram_u16(vol[z:z + 128].cpu().numpy())
-    assert np.array_equal(hist, want)
-    top = vol[nz - 3:].cpu().numpy()
-    bins = O.artifact_bins_u16(top)
-    lut = O.lut_u16(bins)
-    assert np.array_equal(res.lut.cpu().numpy(), lut)
-    rng = np.random.default_rng(3)
-    for s, l in plan.scheme_level.items():
-        sp = schemes[s]
-        atl = res.atlases[s]
-        b = 1 << l
-        for _ in range(2000 // 4):
-            kz, y, x = (int(rng.integers(0, nz >> l)), int(rng.integers(0, ny >> l)), int(rng.integers(0, nx >> l)))
-            blk = vol[kz * b:(kz + 1) * b, y * b:(y + 1) * b, x * b:(x + 1) * b].cpu().numpy()
-            f = lut[np.minimum(blk, 4095)].astype(np.int64)
-            cnt = b ** 3
-            expect = (2 * int(f.sum()) + cnt) // (2 * cnt)          # volume.py:306-308
-            m, w = divmod(kz, sp.grid * sp.grid)
-            cy, cx = divmod(w, sp.grid)
-            got = int(atl[m, cy * sp.s + y, cx * sp.s + x].item())
-            assert got == expect, (s, kz, y, x)
+    got = {s: res.atlases[s].cpu().numpy() for s in schemes}
+    got_hist, got_lut = res.hist.cpu().numpy(), res.lut.cpu().numpy()
+    del res
+    hist, bins, lut, levels = _chunked_oracle(vol, 4)
     del vol
     torch.cuda.empty_cache()
+    assert np.array_equal(got_hist, hist)
+    assert np.array_equal(got_lut, lut)
+    for s, l in plan.scheme_level.items():
+        sp = schemes[s]
+        want = np.stack(O.encode_slicemaps(O.pad_to_cube(levels[l], s), (sp.s, sp.atlas_dim, sp.grid, sp.map_count)))
+        assert np.array_equal(got[s], want), s
 
 
 def test_artifact_lut_single_launch(P, cuda):
@@ -504,34 +526,75 @@ def test_acceptance_snapshot_36_views(P, golden, golden_dp):
 
 # ---------------------------------------------------------------- config 5 stream (extension)
 
+def _c5_expected(levels, ps):
+    """Per level: _scheme_volume (any ratio) + _pad_to_cube + encode (pipeline.py:215-237,
+    slicemap.py:120-142) with the stream's planned scheme."""
+    out = {}
+    for l, sp in ps.levels.items():
+        tx, ty, tz = ps.targets[l]
+        src = O.downscale(levels[l], (tx, ty, tz))
+        out[l] = np.stack(O.encode_slicemaps(O.pad_to_cube(src, sp.s), (sp.s, sp.atlas_dim, sp.grid, sp.map_count)))
+    return out
+
+
 def test_stream_c5_shape_reduced(P, cuda):
-    """Config-5 processing (u16 anisotropic, levels -> padded atlases, 36-view MIP
-    strip) at 1/8 scale against the oracle: histogram, LUT and every atlas
-    bit-exact, thumbnails within 1/255."""
+    """Config-5 processing at reduced scale (u16 anisotropic, planned schemes, levels
+    -> padded atlases, 6-view MIP strip) against the oracle: histogram, LUT and every
+    atlas bit-exact, thumbnails within 1/255; and round 1's pow2-1024 variant."""
     from paper_2311_15038_b200 import synth
-    from paper_2311_15038_b200.stream import PreviewStream, scheme_for
+    from paper_2311_15038_b200.stream import PreviewStream, scheme_pow2
     spec = synth.small((256, 192, 192), dtype="u16", seed=21, n_shells=4)
     vol = synth.generate(spec, device=cuda)
-    ps = PreviewStream(spec.shape, torch.uint16, thumb_dim=64, n_views=6, device=cuda)
-    res = ps.process(vol)
     vox = vol.cpu().numpy()
     hist, bins, f, _, _ = O.preview_pipeline(vox, [])
-    assert np.array_equal(res.hist.cpu().numpy(), hist)
-    assert set(np.nonzero(res.flags.cpu().numpy())[0].tolist()) == set(bins)
     nz, ny, nx = vox.shape
-    for l, sp in ps.levels.items():
-        lv = O.downscale(f, (nx >> l, ny >> l, nz >> l))
-        want = np.stack(O.encode_slicemaps(O.pad_to_cube(lv, sp.s), (sp.s, sp.atlas_dim, sp.grid, sp.map_count)))
-        assert np.array_equal(res.atlases[l].cpu().numpy(), want), l
-        if l == ps.thumb_level:
-            thumb_src = lv
-    assert ps.thumb_shape == thumb_src.shape
-    for k, view in enumerate(ps.views):
-        ref = O.render_mip(thumb_src, view.azimuth_deg, view.image_dim, view.steps)
-        got = res.thumbs[k].cpu().numpy()
-        assert int(np.abs(got[..., 0].astype(int) - ref).max()) <= 1
-        assert (got[..., 3] == 255).all()
-    assert scheme_for((1024, 768, 768)) == (1024, 4096, 4, 64) or scheme_for((1024, 768, 768)).s == 1024
+    levels = {l: O.downscale(f, (nx >> l, ny >> l, nz >> l)) for l in range(1, 5)}
+    for variant in ("scheme", "pow2-1024"):
+        ps = PreviewStream(spec.shape, torch.uint16, thumb_dim=64, n_views=6, device=cuda, variant=variant)
+        res = ps.process(vol)
+        assert np.array_equal(res.hist.cpu().numpy(), hist)
+        assert set(np.nonzero(res.flags.cpu().numpy())[0].tolist()) == set(bins)
+        for l, want in _c5_expected(levels, ps).items():
+            assert np.array_equal(res.atlases[l].cpu().numpy(), want), (variant, l)
+        thumb_src = levels[ps.thumb_level]
+        assert ps.thumb_shape == thumb_src.shape
+        for k, view in enumerate(ps.views):
+            ref = O.render_mip(thumb_src, view.azimuth_deg, view.image_dim, view.steps)
+            got = res.thumbs[k].cpu().numpy()
+            assert int(np.abs(got[..., 0].astype(int) - ref).max()) <= 1
+            assert (got[..., 3] == 255).all()
+    assert scheme_pow2((1024, 768, 768)) == (1024, 4096, 4, 64)
+
+
+def test_stream_c5_full_shape_every_atlas_byte(P, cuda):
+    """Config 5 at its real shape (1536^2 x 2048 12-bit u16, 9 GiB) with SURVEY s8(d)'s
+    composition: L1 768^2 x 1024 -> 512^3 through the general 1.5:1 / 2:1 downscale,
+    L2..L4 identity + zero pad into the planned 512 / 256 / 128 schemes.  Histogram,
+    LUT and EVERY atlas byte against the chunked oracle; the MIP strip's first view on
+    sampled rows against the oracle within 1/255."""
+    import torch
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.stream import PreviewStream
+    spec = synth.config("c5")
+    vol = synth.generate(spec, device=cuda)
+    ps = PreviewStream(spec.shape, torch.uint16, device=cuda)
+    assert {l: sp.s for l, sp in ps.levels.items()} == {1: 512, 2: 512, 3: 256, 4: 128}
+    assert ps.targets[1] == (512, 512, 512) and ps.targets[2] == (384, 384, 512)
+    res = ps.process(vol)
+    got = {l: t.cpu().numpy() for l, t in res.atlases.items()}
+    got_hist, got_flags = res.hist.cpu().numpy(), res.flags.cpu().numpy()
+    thumbs = res.thumbs.cpu().numpy()
+    hist, bins, lut, levels = _chunked_oracle(vol, 4)
+    del vol, res
+    torch.cuda.empty_cache()
+    assert np.array_equal(got_hist, hist)
+    assert set(np.nonzero(got_flags)[0].tolist()) == set(bins)
+    for l, want in _c5_expected(levels, ps).items():
+        assert np.array_equal(got[l], want), l
+    v0 = ps.views[0]
+    for r0 in (100, 300):
+        ref = O.render_mip(levels[ps.thumb_level], v0.azimuth_deg, v0.image_dim, v0.steps, rows=(r0, r0 + 2))
+        assert int(np.abs(thumbs[0, r0:r0 + 2, :, 0].astype(int) - ref).max()) <= 1, r0
 
 
 def test_apply_circle_mask_golden(P, golden_dp):
@@ -548,22 +611,35 @@ def test_apply_circle_mask_golden(P, golden_dp):
         P.apply_circle_mask(vol, C(cx=3.0, cy=1.0, r=5.0), margin=1.0)
 
 
-def test_c4_full_size_mip_rows_vs_exact_path(P, cuda):
-    """Config 4 at full size (1024^3, 1024^2, 3548 steps): the fp32 row-plane MIP and
-    the texture-gather alpha path agree within 1/255 with the fp64 path (bit-exact
-    to the oracle on every small case) on sampled image rows of 3 azimuths."""
+def test_c4_full_size_rows_vs_oracle(P, cuda):
+    """Config 4 at full size (1024^3, 1024^2, 3548 steps, 3 azimuths): sampled image
+    rows of the fp32 MIP and alpha paths within 1/255 of the ORACLE (render_mip /
+    render_alpha restricted to those rows), the fp64 additive path (the reference's
+    own mode) bit-exact to the oracle's render_view on the same rows."""
     import math
     from paper_2311_15038_b200 import device as dev, synth
     spec = synth.config("c4")
     vol = synth.generate(spec, device=cuda)
+    vox = vol.cpu().numpy()
     steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * spec.shape[0])
-    for mode in ("mip", "alpha"):
+    tf = P.ViewParams(mode="alpha").tf
+    rows = ((130, 132), (505, 507), (880, 882))
+    for mode in ("mip", "alpha", "additive"):
         views = [P.ViewParams(azimuth_deg=a, image_dim=1024, steps=steps, mode=mode) for a in (0.0, 37.0, 250.0)]
-        fast = dev.render(vol, views, channels=4, fp32=True).cpu().numpy()
-        for r0 in (130, 505, 880):
-            exact = dev.render(vol, views, channels=4, fp32=False, rows=(r0, r0 + 6)).cpu().numpy()
-            d = np.abs(fast[:, r0:r0 + 6].astype(int) - exact.astype(int))
-            assert int(d.max()) <= 1, (mode, r0, int(d.max()))
+        fp32 = mode != "additive"
+        img = dev.render(vol, views, channels=4 if fp32 else 1, fp32=fp32).cpu().numpy()
+        for k, v in enumerate(views):
+            for r in rows:
+                if mode == "mip":
+                    ref = O.render_mip(vox, v.azimuth_deg, 1024, steps, rows=r)
+                    d = np.abs(img[k, r[0]:r[1], :, 0].astype(int) - ref.astype(int))
+                elif mode == "alpha":
+                    ref = O.render_alpha(vox, v.azimuth_deg, 1024, steps, tf, 0.99, rows=r)
+                    d = np.abs(img[k, r[0]:r[1]].astype(int) - ref.astype(int))
+                else:
+                    ref = O.render_view(vox, v.azimuth_deg, 1024, steps, "additive", rows=r)
+                    d = np.abs(img[k, r[0]:r[1]].astype(int) - ref.astype(int))
+                assert int(d.max()) <= (0 if mode == "additive" else 1), (mode, v.azimuth_deg, r, int(d.max()))
     del vol
     torch.cuda.empty_cache()
 
