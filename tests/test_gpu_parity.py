@@ -563,7 +563,8 @@ def test_stream_c5_shape_reduced(P, cuda):
             got = res.thumbs[k].cpu().numpy()
             assert int(np.abs(got[..., 0].astype(int) - ref).max()) <= 1
             assert (got[..., 3] == 255).all()
-    assert scheme_pow2((1024, 768, 768)) == (1024, 4096, 4, 64)
+    sp = scheme_pow2((1024, 768, 768))
+    assert (sp.s, sp.atlas_dim, sp.grid, sp.map_count) == (1024, 4096, 4, 64)
 
 
 def test_stream_c5_full_shape_every_atlas_byte(P, cuda):
