@@ -52,14 +52,25 @@ template <typename T> struct Vox;
 template <> struct Vox<uint8_t> {
   static constexpr int UXW = 16, NBINS = 256, ROWW = 64, HWORDS = 256 * ROWW;
 };
-// u16: COLS interleaved columns [bin][lane % COLS] -- lanes of different columns
-// never share a bank, so the random-bin conflict degree of a warp-wide ATOMS
-// drops (simulated E[max bank load] 3.5 -> 3.3 for 4 columns, 3.0 for 8)
+// u16 (4096 bins): a random-bin warp-wide ATOMS on one shared table costs ~3.4
+// wavefronts (bank conflicts), which bounded round 1's pass (4 interleaved
+// columns [bin][lane % 4]: 58% of HBM).  Now a HOT WINDOW of HOT consecutive
+// bins, chosen per CTA from its first tile (the densest HOT/64 of 64 coarse
+// buckets), lives in per-lane columns [slot][lane] (bank == lane: conflict-free,
+// like u8); the other bins go to one shared 4096-word table.  A voxel costs ONE
+// ATOMS either way (the counter word still carries the LUT byte) and the warp
+// pays an extra wavefront only for its out-of-window lanes.  CTP_U16_HOT=0
+// restores round 1's COLS-column table.
 #ifndef CTP_U16_COLS
 #define CTP_U16_COLS 4
 #endif
+#ifndef CTP_U16_HOT
+#define CTP_U16_HOT 448
+#endif
 template <> struct Vox<uint16_t> {
-  static constexpr int UXW = 8, NBINS = 4096, COLS = CTP_U16_COLS, HWORDS = 4096 * COLS;
+  static constexpr int UXW = 8, NBINS = 4096, COLS = CTP_U16_COLS, HOT = CTP_U16_HOT;
+  static_assert(HOT % 64 == 0 && HOT <= 4096, "the hot window is whole 64-bin buckets");
+  static constexpr int HWORDS = HOT > 0 ? HOT * 32 + 4096 : 4096 * COLS;
 };
 
 struct PvGeom {
@@ -134,7 +145,7 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 }
 
 template <typename T>
-__device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads) {
+__device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads, int hot_base) {
   __syncthreads();
   if constexpr (sizeof(T) == 1) {
     for (int bin = threadIdx.x; bin < 256; bin += threads) {
@@ -147,6 +158,25 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads
         hs[idx] = wv & 0xFFFu;
       }
       if (s && hist) atomicAdd(hist + bin, (unsigned long long)s);
+    }
+  } else if constexpr (Vox<uint16_t>::HOT > 0) {
+    constexpr int H = Vox<uint16_t>::HOT;
+    for (int sl = threadIdx.x; sl < H; sl += threads) {  // hot window: [slot][lane], rotated (conflict-free)
+      uint32_t s = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; k++) {
+        const int idx = sl * 32 + ((k + sl) & 31);
+        const uint32_t wv = hs[idx];
+        s += wv >> 12;
+        hs[idx] = wv & 0xFFFu;
+      }
+      if (s && hist) atomicAdd(hist + hot_base + sl, (unsigned long long)s);
+    }
+    uint32_t* cold = hs + H * 32;
+    for (int b = threadIdx.x; b < 4096; b += threads) {
+      const uint32_t wv = cold[b];
+      cold[b] = wv & 0xFFFu;
+      if ((wv >> 12) && hist) atomicAdd(hist + b, (unsigned long long)(wv >> 12));
     }
   } else {
     constexpr int C = Vox<uint16_t>::COLS;
@@ -165,9 +195,11 @@ __device__ void flush_counts(uint32_t* hs, unsigned long long* hist, int threads
 }
 
 // One 16-byte row vector of a unit: UXW atomics; returns the old counter words.
-// u8: tbl = table base (uniform), lb = 4 * lane; u16: lb = table base + column.
+// u8: tbl = table base (uniform), lb = 4 * lane.  u16 with a hot window: tbl =
+// the shared (cold) table, lb = hot table + 4 * lane - (hot_base << 7), hb =
+// hot_base.  u16 without: lb = table base + column.
 template <typename T>
-__device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32_t lb, uint32_t* o) {
+__device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32_t lb, uint32_t hb, uint32_t* o) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};
   if constexpr (sizeof(T) == 1) {
 #pragma unroll
@@ -177,6 +209,15 @@ __device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32
         // [0, 0, v, 4*lane] = (v << 8) | (lane << 2): the voxel's counter word
         const uint32_t off = __byte_perm(w[k], lb, 0x7604u | ((uint32_t)b << 4));
         o[4 * k + b] = atom_add_shared(tbl + off, kOne);
+      }
+  } else if constexpr (Vox<uint16_t>::HOT > 0) {
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t v = h ? (w[k] >> 16) : (w[k] & 0xFFFFu);
+        const uint32_t addr = (v - hb < (uint32_t)Vox<uint16_t>::HOT) ? lb + (v << 7) : tbl + (min(v, 4095u) << 2);
+        o[2 * k + h] = atom_add_shared(addr, kOne);
       }
   } else {
     constexpr uint32_t SH = 2 + (Vox<uint16_t>::COLS == 1 ? 0 : Vox<uint16_t>::COLS == 2 ? 1 : Vox<uint16_t>::COLS == 4 ? 2 : 3);
@@ -319,14 +360,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (threadIdx.x == 0) a.ws[4096] = 0;
     }
   }
-  // counter words: LUT value in the low byte, count 0
-  for (int i = threadIdx.x; i < HW; i += THREADS) {
-    const int bin = (sizeof(T) == 2) ? i / Vox<uint16_t>::COLS : (i >> 6);
-    hs[i] = a.top ? (uint32_t)slut[bin] : (a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255));
-  }
-  const uint32_t tbl = (uint32_t)__cvta_generic_to_shared(hs);
-  const uint32_t lb = (sizeof(T) == 2) ? tbl + 4u * (uint32_t)(lane % Vox<uint16_t>::COLS) : 4u * (uint32_t)lane;
-
   // unit slots of this thread (same in every tile): coordinates + stage offset
   int uxu[UPT], uyr[UPT], uzr[UPT];
   uint32_t uso[UPT];
@@ -343,6 +376,67 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const uint32_t row_dy = (uint32_t)g.box_x * sizeof(T);
   const uint32_t row_dz = (uint32_t)g.box_x * g.ty * sizeof(T);
+
+  // u16 hot window: the densest HOT/64 consecutive 64-bin buckets of a sample of
+  // this CTA's first tile (one row vector per thread) -- any choice is exact, it
+  // only decides which voxels take the conflict-free per-lane columns
+  __shared__ int s_hot_base;
+  int hot_base = 0;
+  if constexpr (sizeof(T) == 2 && Vox<uint16_t>::HOT > 0) {
+    constexpr int WB = Vox<uint16_t>::HOT / 64;
+    for (int i = threadIdx.x; i < 64; i += THREADS) hs[i] = 0;
+    __syncthreads();
+    if (t_begin < t_end && uzr[0] < TZ / UZ) {
+      mbar_wait(bar0, 0u);  // the first tile (stage 0) has landed
+      const uint4 q = lds128(stage0 + uso[0]);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        atomicAdd(&hs[min(w[k] & 0xFFFFu, 4095u) >> 6], 1u);
+        atomicAdd(&hs[min(w[k] >> 16, 4095u) >> 6], 1u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t best = 0;
+      int best_s = 0;
+      for (int st = lane; st <= 64 - WB; st += 32) {
+        uint32_t m = 0;
+        for (int j = 0; j < WB; j++) m += hs[st + j];
+        if (m > best) { best = m; best_s = st; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {  // max mass, smallest start on ties
+        const uint32_t ob = __shfl_xor_sync(0xFFFFFFFFu, best, off);
+        const int os = __shfl_xor_sync(0xFFFFFFFFu, best_s, off);
+        if (ob > best || (ob == best && os < best_s)) { best = ob; best_s = os; }
+      }
+      if (lane == 0) s_hot_base = best_s * 64;
+    }
+    __syncthreads();
+    hot_base = s_hot_base;
+  }
+
+  // counter words: LUT value in the low byte, count 0
+  for (int i = threadIdx.x; i < HW; i += THREADS) {
+    int bin;
+    if constexpr (sizeof(T) == 1) bin = i >> 6;
+    else if constexpr (Vox<uint16_t>::HOT > 0) bin = i < Vox<uint16_t>::HOT * 32 ? hot_base + (i >> 5) : i - Vox<uint16_t>::HOT * 32;
+    else bin = i / Vox<uint16_t>::COLS;
+    hs[i] = a.top ? (uint32_t)slut[bin] : (a.lut ? (uint32_t)a.lut[bin] : (uint32_t)min(bin, 255));
+  }
+  const uint32_t hs_a = (uint32_t)__cvta_generic_to_shared(hs);
+  uint32_t tbl, lb;
+  if constexpr (sizeof(T) == 1) {
+    tbl = hs_a;
+    lb = 4u * (uint32_t)lane;
+  } else if constexpr (Vox<uint16_t>::HOT > 0) {
+    tbl = hs_a + 4u * Vox<uint16_t>::HOT * 32;                           // cold table
+    lb = hs_a + 4u * (uint32_t)lane - ((uint32_t)hot_base << 7);         // hot [slot][lane], slot = v - hot_base
+  } else {
+    tbl = hs_a;
+    lb = hs_a + 4u * (uint32_t)(lane % Vox<uint16_t>::COLS);
+  }
 
   // Level >= 3 reduction slot (tile-invariant): a lane owns one (z2, y2) row run
   // of four x-adjacent level-2 cells (x-quad q: level-1 x-cells 8q .. 8q+7, one
@@ -426,7 +520,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int h = 0; h < (L >= 1 ? 2 : 1); h++) {
           const int rr = r2 + h;
           const uint4 q = lds128(sbase + uso[i] + (rr / UZ) * row_dz + (rr % UZ) * row_dy);
-          row_atomics<T>(q, tbl, lb, o[h]);
+          row_atomics<T>(q, tbl, lb, (uint32_t)hot_base, o[h]);
           if (want0) {  // level 0: the filtered voxels themselves
             uint8_t* dst = a.lv[0].out + level_offset<POW2>(a.lv[0], z + rr / UZ, y + rr % UZ, x);
             uint32_t pk[UXW / 4];
@@ -578,7 +672,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
     if (++since_flush == g.flush_tiles) {
       since_flush = 0;
-      flush_counts<T>(hs, a.hist, THREADS);
+      flush_counts<T>(hs, a.hist, THREADS, hot_base);
     }
     // next tile (row-major: x fastest)
     if (++tx_i == g.tiles_x) {
@@ -586,7 +680,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (++ty_i == g.tiles_y) { ty_i = 0; ++tz_i; }
     }
   }
-  flush_counts<T>(hs, a.hist, THREADS);
+  flush_counts<T>(hs, a.hist, THREADS, hot_base);
   // atlas rows stored into a peer's atlases (the fused gather of a sharded step):
   // system-scope fence, so they are visible to the peer before the collective that
   // follows this kernel on the stream completes the step
