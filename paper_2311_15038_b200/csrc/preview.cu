@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     tbl = hs_a;
     lb = 4u * (uint32_t)lane;
   } else if constexpr (Vox<uint16_t>::HOT > 0) {
-    tbl = hs_a + 4u * Vox<uint16_t>::HOT * 32;                           // cold table
+    // (an opaque copy: keeps the cold-table base in one register, a cold address is one IMAD/LEA)
+    asm volatile("mov.u32 %0, %1;" : "=r"(tbl) : "r"(hs_a + 4u * Vox<uint16_t>::HOT * 32));  // cold table
     lb = hs_a + 4u * (uint32_t)lane - ((uint32_t)hot_base << 7);         // hot [slot][lane], slot = v - hot_base
   } else {
     tbl = hs_a;
