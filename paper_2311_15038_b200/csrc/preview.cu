@@ -65,7 +65,7 @@ template <> struct Vox<uint8_t> {
 #define CTP_U16_COLS 4
 #endif
 #ifndef CTP_U16_HOT
-#define CTP_U16_HOT 448
+#define CTP_U16_HOT 512
 #endif
 template <> struct Vox<uint16_t> {
   static constexpr int UXW = 8, NBINS = 4096, COLS = CTP_U16_COLS, HOT = CTP_U16_HOT;
@@ -212,13 +212,15 @@ __device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32
       }
   } else if constexpr (Vox<uint16_t>::HOT > 0) {
 #pragma unroll
-    for (int k = 0; k < 4; k++)
+    for (int k = 0; k < 4; k++) {
+      const uint32_t wc = __vminu2(w[k], 0x0FFF0FFFu);  // both voxels saturated to 4095 (VIMNMX.U16x2)
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const uint32_t v = h ? (w[k] >> 16) : (w[k] & 0xFFFFu);
-        const uint32_t addr = (v - hb < (uint32_t)Vox<uint16_t>::HOT) ? lb + (v << 7) : tbl + (min(v, 4095u) << 2);
+        const uint32_t v = __byte_perm(wc, 0u, h ? 0x4432u : 0x4410u);  // one PRMT per voxel
+        const uint32_t addr = (v - hb < (uint32_t)Vox<uint16_t>::HOT) ? lb + (v << 7) : tbl + (v << 2);
         o[2 * k + h] = atom_add_shared(addr, kOne);
       }
+    }
   } else {
     constexpr uint32_t SH = 2 + (Vox<uint16_t>::COLS == 1 ? 0 : Vox<uint16_t>::COLS == 2 ? 1 : Vox<uint16_t>::COLS == 4 ? 2 : 3);
 #pragma unroll
@@ -304,7 +306,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < NST; s++)
       if (t_begin + s < t_end) issue(t_begin + s, s);
 
-  __shared__ uint8_t slut[Vox<T>::NBINS];
+  // the LUT of the in-kernel artifact step, until it is copied into the counter words:
+  // u16 (L >= 2) keeps it in the level-1 sum buffers (free until the first tile), so the
+  // 4 KB do not come out of the hot window's budget
+  uint8_t* slut;
+  if constexpr (sizeof(T) == 2 && L >= 2) {
+    static_assert(2 * LY::S1_BYTES >= Vox<T>::NBINS, "the LUT fits the level-1 sum buffers");
+    slut = reinterpret_cast<uint8_t*>(s1);
+  } else {
+    __shared__ uint8_t slut_s[Vox<T>::NBINS];
+    slut = slut_s;
+  }
   if (a.top != nullptr) {
     // ---- the artifact-LUT step inside this launch (mask.py:215-231, 241-245):
     // the first tiles are already streaming in while every CTA histograms its
