@@ -115,6 +115,158 @@ __global__ void __launch_bounds__(256) downscale_u8_vec_kernel(const uint8_t* __
   }
 }
 
+// Warp-per-output-row path (16-byte rows, cells of <= 257 source rows, x cells of
+// <= WMAX columns, the cell tables and one column-sum row per warp in shared
+// memory).  Cell starts (volume.py:265-274) are tabulated once per CTA -- the x
+// table packed as (column-sum index of the cell's first column, width) -- so a
+// row costs no division but jz = row / ty.  Per output row (jz, jy) a warp
+//   1. sums its cell's source rows column-wise: each lane owns 16-byte column
+//      chunks, every source byte read once with a 16-byte load (four in flight),
+//      sums in packed 16-bit lanes (even / odd bytes);
+//   2. writes the 16 column sums of each chunk with four 16-byte stores to a
+//      column-sum row laid out as idx(x) = x + 4 * (x >> 5) -- chunk c starts at
+//      word 16c + 4(c >> 1), so the 8 lanes of a 16-byte-store phase hit 8
+//      distinct 4-bank groups (conflict-free);
+//   3. sums each output's x cell from there (WMAX predicated reads) and rounds
+//      half up, floor((2 acc + cnt) / (2 cnt)) (volume.py:306-308), with a
+//      per-row magic multiplier per cell width (exact while 2 cnt < 4099), one
+//      byte per lane and output (coalesced stores).
+// No CTA barrier inside the loop: a warp only ever reads its own row.
+constexpr int kDsWarps = 8;
+
+__host__ __device__ __forceinline__ uint32_t ds_idx(uint32_t x) { return x + ((x >> 5) << 2); }
+
+template <int WMAX>
+__global__ void __launch_bounds__(32 * kDsWarps) downscale_u8_warp_kernel(const uint8_t* __restrict__ in, int nz,
+                                                                          int ny, int nx, int tz, int ty, int tx,
+                                                                          uint8_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t dsm[];
+  const int row_words = (int)ds_idx((uint32_t)nx) + 4;  // one column-sum row (16-byte multiple)
+  // per output x (WMAX <= 2): idx(xa) | idx(second column, or of the warp row's zero
+  // word) << 15 | (w - 1) << 30;  (WMAX > 2): idx(xa) | width << 20 | b << 26, b =
+  // columns before the next 32-column boundary (where idx skips its 4 pad words)
+  uint32_t* xt = dsm + kDsWarps * row_words;
+  uint32_t* ys = xt + tx;
+  uint32_t* zs = ys + ty + 1;
+  for (int j = threadIdx.x; j < tx; j += blockDim.x) {
+    const uint32_t xa = cell_start(j, nx, tx), xb = cell_start(j + 1, nx, tx);
+    if constexpr (WMAX <= 2)
+      xt[j] = ds_idx(xa) | ((xb - xa == 2 ? ds_idx(xa + 1) : ds_idx((uint32_t)nx)) << 15) | ((xb - xa - 1) << 30);
+    else
+      xt[j] = ds_idx(xa) | ((xb - xa) << 20) | ((32u - (xa & 31u)) << 26);
+  }
+  for (int w = threadIdx.x; w < kDsWarps; w += blockDim.x) dsm[w * row_words + ds_idx((uint32_t)nx)] = 0u;  // zero words
+  for (int j = threadIdx.x; j <= ty; j += blockDim.x) ys[j] = cell_start(j, ny, ty);
+  for (int j = threadIdx.x; j <= tz; j += blockDim.x) zs[j] = cell_start(j, nz, tz);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* colsum = dsm + warp * row_words;
+  const uint32_t cs_base = (uint32_t)__cvta_generic_to_shared(colsum);
+  const int nc = nx >> 4;
+  const uint32_t rows = (uint32_t)ty * (uint32_t)tz;
+  const uint32_t stride = gridDim.x * kDsWarps;
+  const int64_t slice = (int64_t)ny * nx;
+  for (uint32_t row = blockIdx.x * kDsWarps + warp; row < rows; row += stride) {
+    const uint32_t jz = row / (uint32_t)ty, jy = row - jz * (uint32_t)ty;
+    const uint32_t ya = ys[jy], yb = ys[jy + 1], za = zs[jz], zb = zs[jz + 1];
+    const uint32_t cy = yb - ya, ncell = cy * (zb - za);
+    for (int c = lane; c < nc; c += 32) {
+      uint32_t ev[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
+      const uint8_t* p = in + (int64_t)za * slice + (int64_t)ya * nx + 16 * c;  // source row (za, ya)
+      uint32_t y = 0;                                                           // row within the y cell
+      for (uint32_t r = 0; r < ncell; r += 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {  // the next four cell rows (row-major over (z, y)), predicated
+          q[u] = make_uint4(0, 0, 0, 0);
+          if (r + u < ncell) {
+            q[u] = __ldg(reinterpret_cast<const uint4*>(p));
+            p += nx;
+            if (++y == cy) {
+              y = 0;
+              p += slice - (int64_t)cy * nx;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            ev[i] += w[i] & 0x00FF00FFu;
+            od[i] += (w[i] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+      // columns 4i..4i+3 = (ev lo, od lo, ev hi, od hi)
+      const uint32_t dst = cs_base + 4u * ds_idx(16u * (uint32_t)c);
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * i), "r"(ev[i] & 0xFFFFu),
+                     "r"(od[i] & 0xFFFFu), "r"(ev[i] >> 16), "r"(od[i] >> 16)
+                     : "memory");
+    }
+    __syncwarp();
+    uint8_t* orow = out + (int64_t)row * tx;
+    auto lds = [&](uint32_t idx) -> uint32_t {
+      uint32_t v;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(cs_base + 4u * idx));
+      return v;
+    };
+    if (2u * (uint32_t)WMAX * ncell < 4099u) {
+      // q = floor((2 acc + cnt) / (2 cnt)) by a magic multiplier of den = 2 w ncell: exact
+      // while den < 4099 (num <= 255.5 den, num * (M - 2^32 / den) < 2^32 / den)
+      if constexpr (WMAX <= 2) {
+        uint32_t m1 = 0xFFFFFFFFu / (2u * ncell) + 1u, m2 = 0xFFFFFFFFu / (4u * ncell) + 1u;
+        // opaque: otherwise the compiler folds the select into a division per output
+        asm volatile("mov.u32 %0, %0;" : "+r"(m1));
+        asm volatile("mov.u32 %0, %0;" : "+r"(m2));
+        for (int jx = lane; jx < tx; jx += 32) {
+          const uint32_t e = xt[jx];
+          const uint32_t acc = lds(e & 0x7FFFu) + lds((e >> 15) & 0x7FFFu);
+          const bool two = (e >> 30) != 0u;
+          const uint32_t num = 2u * acc + (two ? 2u : 1u) * ncell;
+          orow[jx] = (uint8_t)__umulhi(num, two ? m2 : m1);
+        }
+      } else {
+        uint32_t mg = (lane >= 1 && lane <= WMAX) ? 0xFFFFFFFFu / (2u * (uint32_t)lane * ncell) + 1u : 0u;
+        asm volatile("mov.u32 %0, %0;" : "+r"(mg));
+        for (int j0 = 0; j0 < tx; j0 += 32) {  // warp-uniform trip count: every lane takes the shuffle
+          const int jx = j0 + lane;
+          const bool live = jx < tx;
+          const uint32_t e = live ? xt[jx] : (1u << 20);
+          const uint32_t i0 = e & 0xFFFFFu, w = (e >> 20) & 63u, b = e >> 26;
+          uint32_t acc = 0;
+#pragma unroll
+          for (int k = 0; k < WMAX; k++)
+            if ((uint32_t)k < w) acc += lds(i0 + k + ((uint32_t)k >= b ? 4u : 0u));
+          const uint32_t m = __shfl_sync(0xFFFFFFFFu, mg, (int)w);
+          if (live) orow[jx] = (uint8_t)__umulhi(2u * acc + w * ncell, m);
+        }
+      }
+    } else {  // large cells: a float estimate corrected to the exact integer quotient
+      for (int jx = lane; jx < tx; jx += 32) {
+        const uint32_t e = xt[jx];
+        uint32_t acc = 0, w;
+        if constexpr (WMAX <= 2) {
+          w = (e >> 30) + 1u;
+          acc = lds(e & 0x7FFFu) + lds((e >> 15) & 0x7FFFu);
+        } else {
+          const uint32_t i0 = e & 0xFFFFFu, b = e >> 26;
+          w = (e >> 20) & 63u;
+          for (uint32_t k = 0; k < w; k++) acc += lds(i0 + k + (k >= b ? 4u : 0u));
+        }
+        const uint32_t cnt = w * ncell, num = 2u * acc + cnt, den = 2u * cnt;
+        uint32_t q = (uint32_t)__fmul_rz((float)num, __frcp_rn((float)den));
+        if ((q + 1) * den <= num) q++;
+        if (q * den > num) q--;
+        orow[jx] = (uint8_t)q;
+      }
+    }
+    __syncwarp();  // the next row rewrites colsum
+  }
+}
+
 // One CTA per atlas row (map m, row R of the atlas): every 16-byte chunk of the
 // row is one slice row segment (slice k = m*grid^2 + (R / s)*grid + C / s, row
 // R % s, columns C % s ..) copied with one 16-byte load and store -- or zero
@@ -269,7 +421,39 @@ int ctp_downscale_u8(const uint8_t* in, int64_t nz, int64_t ny, int64_t nx, int6
   // the vector path needs 16-byte rows, <= 257 source rows per cell (packed 16-bit
   // column sums) and the column sums of one row in shared memory
   const int64_t cell_rows = ((ny + ty - 1) / ty + 1) * ((nz + tz - 1) / tz + 1);
-  if (nx % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 && nx <= 16384 && cell_rows <= 257) {
+  const bool vec_ok = nx % 16 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 && nx <= 16384 && cell_rows <= 257;
+  {
+    // warp-per-row path: kDsWarps column-sum rows + the three cell tables in shared memory
+    const size_t sm = ((size_t)kDsWarps * (ds_idx((uint32_t)nx) + 4) + (size_t)(tx + ty + tz + 2)) * sizeof(uint32_t);
+    static const bool force_old = [] { const char* e = getenv("CTP_DOWNSCALE_OLD"); return e && e[0] == '1'; }();
+    int64_t wx = 0;  // widest x cell (volume.py:265-274 starts, the kernel's 32-bit formula)
+    for (int64_t j = 0, prev = 0; j < tx; j++) {
+      const int64_t nxt = (j + 1 >= tx) ? nx : (2 * (j + 1) * nx - tx + 2 * tx - 1) / (2 * tx);
+      if (nxt - prev > wx) wx = nxt - prev;
+      prev = nxt;
+    }
+    if (vec_ok && sm <= 200 * 1024 && wx <= 16 && !force_old) {
+      const int64_t rows = ty * tz;
+      auto go = [&](auto kern) -> int {
+        if (sm > 48 * 1024)
+          CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        int per_sm = 0;
+        CTP_CUDA_CALL(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kDsWarps, sm));
+        if (per_sm < 1) per_sm = 1;
+        int64_t blocks = (rows + kDsWarps - 1) / kDsWarps;
+        if (blocks > (int64_t)per_sm * num_sms()) blocks = (int64_t)per_sm * num_sms();
+        kern<<<(unsigned)blocks, 32 * kDsWarps, sm, st>>>(in, (int)nz, (int)ny, (int)nx, (int)tz, (int)ty, (int)tx,
+                                                           out);
+        CTP_CUDA_CHECK_LAUNCH("downscale_u8_warp_kernel");
+        return CTP_OK;
+      };
+      if (wx <= 2) return go(downscale_u8_warp_kernel<2>);
+      if (wx <= 4) return go(downscale_u8_warp_kernel<4>);
+      if (wx <= 8) return go(downscale_u8_warp_kernel<8>);
+      return go(downscale_u8_warp_kernel<16>);
+    }
+  }
+  if (vec_ok) {
     int tpr = 32;  // threads per output row: one 16-byte column chunk each, <= 256
     while (tpr < 256 && tpr * 16 < nx) tpr *= 2;
     const int rpc = 256 / tpr;

@@ -149,7 +149,10 @@ def test_downscale_vector_path_general_ratios(P, cuda):
     # targets are (tx, ty, tz), shapes (nz, ny, nx) as everywhere in the reference
     for shape, target in [((40, 36, 64), (37, 23, 17)), ((64, 48, 160), (128, 7, 5)), ((256, 256, 32), (2, 16, 16)),
                           ((16, 16, 4096), (999, 16, 1)), ((33, 70, 4096), (999, 3, 1)), ((17, 255, 48), (48, 16, 17)),
-                          ((8, 8, 16384), (5000, 8, 8))]:
+                          ((8, 8, 16384), (5000, 8, 8)),
+                          # the warp-per-row kernel's x-cell classes: <= 2 (1.5:1 / 1.33:1, config 5), <= 4, <= 8
+                          ((64, 48, 96), (64, 32, 32)), ((48, 40, 1024), (768, 30, 36)), ((40, 24, 320), (94, 7, 13)),
+                          ((24, 20, 256), (37, 20, 24))]:
         v = rng.integers(0, 256, size=shape, dtype=np.uint8)
         v[:, :, :16] = 255  # saturated columns: the packed lanes at their maximum
         got = dev.downscale(torch.from_numpy(v).to(cuda), target).cpu().numpy()
