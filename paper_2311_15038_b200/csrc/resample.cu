@@ -170,24 +170,25 @@ __global__ void __launch_bounds__(32 * kDsWarps) downscale_u8_warp_kernel(const 
     const uint32_t jz = row / (uint32_t)ty, jy = row - jz * (uint32_t)ty;
     const uint32_t ya = ys[jy], yb = ys[jy + 1], za = zs[jz], zb = zs[jz + 1];
     const uint32_t cy = yb - ya, ncell = cy * (zb - za);
+    const uint8_t* row0 = in + (int64_t)za * slice + (int64_t)ya * nx;  // source row (za, ya)
     for (int c = lane; c < nc; c += 32) {
       uint32_t ev[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
-      const uint8_t* p = in + (int64_t)za * slice + (int64_t)ya * nx + 16 * c;  // source row (za, ya)
-      uint32_t y = 0;                                                           // row within the y cell
+      uint32_t y = 0, z = 0;  // next cell row (row-major over (z, y))
       for (uint32_t r = 0; r < ncell; r += 4) {
-        uint4 q[4];
+        // the next four cell rows' offsets first (no memory dependence), then four loads in flight
+        int64_t off[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {  // the next four cell rows (row-major over (z, y)), predicated
-          q[u] = make_uint4(0, 0, 0, 0);
-          if (r + u < ncell) {
-            q[u] = __ldg(reinterpret_cast<const uint4*>(p));
-            p += nx;
-            if (++y == cy) {
-              y = 0;
-              p += slice - (int64_t)cy * nx;
-            }
+        for (int u = 0; u < 4; u++) {
+          off[u] = (int64_t)z * slice + (int64_t)y * nx;
+          if (++y == cy) {
+            y = 0;
+            ++z;
           }
         }
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          q[u] = (r + u < ncell) ? __ldg(reinterpret_cast<const uint4*>(row0 + off[u] + 16 * c)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
@@ -221,12 +222,20 @@ __global__ void __launch_bounds__(32 * kDsWarps) downscale_u8_warp_kernel(const 
         // opaque: otherwise the compiler folds the select into a division per output
         asm volatile("mov.u32 %0, %0;" : "+r"(m1));
         asm volatile("mov.u32 %0, %0;" : "+r"(m2));
-        for (int jx = lane; jx < tx; jx += 32) {
-          const uint32_t e = xt[jx];
+        auto one = [&](uint32_t e) -> uint32_t {
           const uint32_t acc = lds(e & 0x7FFFu) + lds((e >> 15) & 0x7FFFu);
           const bool two = (e >> 30) != 0u;
-          const uint32_t num = 2u * acc + (two ? 2u : 1u) * ncell;
-          orow[jx] = (uint8_t)__umulhi(num, two ? m2 : m1);
+          return __umulhi(2u * acc + (two ? 2u : 1u) * ncell, two ? m2 : m1);
+        };
+        if (((tx & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 3) == 0)) {
+          // 4 consecutive outputs per lane: one 16-byte table load, one 4-byte store
+          for (int j4 = lane; 4 * j4 < tx; j4 += 32) {
+            const uint4 e = *reinterpret_cast<const uint4*>(xt + 4 * j4);
+            *reinterpret_cast<uint32_t*>(orow + 4 * j4) =
+                one(e.x) | (one(e.y) << 8) | (one(e.z) << 16) | (one(e.w) << 24);
+          }
+        } else {
+          for (int jx = lane; jx < tx; jx += 32) orow[jx] = (uint8_t)one(xt[jx]);
         }
       } else {
         uint32_t mg = (lane >= 1 && lane <= WMAX) ? 0xFFFFFFFFu / (2u * (uint32_t)lane * ncell) + 1u : 0u;

@@ -1,4 +1,5 @@
-# general-ratio downscale: warp-per-row kernel vs round 1's (CTP_DOWNSCALE_OLD=1), then the parity tests
+# general-ratio downscale (ctp_downscale_u8): the warp-per-row kernel vs round 1's (CTP_DOWNSCALE_OLD=1),
+# clocks warmed up for 1 s before each timing, then the parity tests
 set -u
 for a in "--c5" "--target 512" "--target 768" "--target 300" "--target 1000"; do
   python tools/prof_downscale.py $a
