@@ -3,26 +3,31 @@
 Headline workload = BASELINE config 2: a 1024^3 uint8 volume (seeded synthetic
 stand-in for a NOVA scan).  One step = volume_histogram + artifact_bins +
 filter_histogram_bins + the 512^3/256^3/128^3 levels (each direct from the
-filtered volume) + their slicemap atlases (8x4096^2, 4x2048^2, 2x1024^2):
-ONE cooperative launch (artifact-LUT phase, grid barrier, fused pass).
-  value  = GVoxel/s with the volume resident in HBM (1 GiB > 126 MB L2, so no flush)
-  e2e    = the same through the host-buffer session (pinned host volume in,
-           pinned host atlases + histogram out, PCIe copies inside the timed region)
-  mip    = config-4 MIP frames/s (36 azimuths, 1024^2 RGBA8, 0.5-voxel steps, 1024^3)
+filtered volume) + their slicemap atlases (8x4096^2, 4x2048^2, 2x1024^2).
+  value  = GVoxel/s of ONE volume per step, resident in HBM (1 GiB > 126 MB L2:
+           no flush needed).  N = 1: one cooperative launch per step (artifact-LUT
+           phase, grid barrier, fused pass).  N > 1 (torchrun): the same volume
+           z-slab sharded (strong scaling): LUT from the top-slab
+           owner (all-reduce), every rank's fused pass storing its atlas cell rows
+           straight into rank 0's atlases over NVLink (CUDA IPC peer mapping,
+           system-scope fence), int64 histogram all-reduce (NCCL).
+  e2e    = the same composition through the REFERENCE-FACING calls: ctprev's own
+           namespace after install() (volume_histogram, artifact_bins,
+           filter_histogram_bins, downscale_volume x3, encode_slicemaps x3) on a
+           pageable host Volume, fresh host arrays out, every upload / read-back
+           inside the timed region.  Side keys: PreviewSession (pinned, streamed)
+           and ctprev's build_interactive_preview after install().
+  mip    = config-4 MIP frames/s (36 azimuths, 1024^2 RGBA8, 0.5-voxel steps,
+           1024^3); N > 1: image rows split with the volume replicated (+ sort-last
+           z-slab bands and replicas as side keys).
+N > 1 side keys: "replicas" (one c2 volume per rank, weak) and "c3_zslab"
+(config 3, one 16 GiB u16 volume z-slab sharded).  N = 1 side keys under
+"other_configs": c1, c3, c4 alpha / additive, c5, ingest, PNG.
 
-Multi-GPU (torchrun, --gpus N): the headline is weak -- every GPU reduces its
-own c2 scan (independent objects, no data-path collective), value = all ranks'
-voxels / the slowest rank's time.  Side measurement "c2_zslab" (strong): ONE
-1024^3 volume split into N z-slabs (heights whole 2^3 cells and atlas cell
-rows, no halo): the artifact LUT broadcast from the rank holding the top
-slices, histograms all-reduced (NCCL), and every rank's fused pass storing its
-atlas cell rows straight into rank 0's atlases through a CUDA IPC mapping over
-NVLink -- the gather is part of the pass (paper_2311_15038_b200/dist.py).
-MIP likewise: replicas (headline) and "sort_last" (one volume, z-slab bands
-stored into rank 0's images by the render kernels).
-
-``--impl reference``: the reference's CPU algorithm (the numpy oracle port of
-ctprev) on the box's host cores, process pool over z-slabs, bounded sample.
+``--impl reference`` (bench_ref.py): ctprev's OWN functions (baseline/_ref) on the
+box's host cores -- the same composition fanned out over z-slabs on a process
+pool, plus an as-is single-process sample and render_view -- with the same
+config dict; never this package or its .so.
 """
 from __future__ import annotations
 
@@ -166,6 +171,7 @@ def main():
     from paper_2311_15038_b200.pipeline import PreviewSession, plan_preview
     from paper_2311_15038_b200.types import plan_scheme
 
+    import bench_ref  # the shared headline config (numpy only)
     _lib.load()
     spec = synth.config("c2")
     nz, ny, nx = spec.shape
@@ -173,11 +179,14 @@ def main():
     plan = plan_preview(spec.shape, schemes)
     assert not plan.general and plan.nlev == 3
     level_of = dict(plan.scheme_level)
-    # headline: every GPU reduces its own c2 scan (N > 1: independent scans, weak scaling, no
-    # data-path collective); the z-slab sharding of ONE volume across the N GPUs is the
-    # side measurement "c2_zslab" below
-    sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), 0, 1, device)
-    slab = synth.generate(synth.config("c2", seed=rank), device=device)  # this GPU's scan
+    # headline: ONE c2 volume per step, z-slab sharded across the N ranks (strong scaling; N = 1:
+    # the whole volume, one cooperative launch per step).  N > 1: the LUT from
+    # the top-slab owner (all-reduce, so no rank stores into rank 0's reused atlases early), the
+    # fused pass per slab storing its atlas rows straight into rank 0's atlases over NVLink
+    # (CUDA IPC peer mapping, system-scope fence), the int64 histogram all-reduce
+    sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), rank, world,
+                        device, peer_atlases=world > 1)
+    slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)  # this rank's slab
     stream = torch.cuda.current_stream()
     k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -218,7 +227,7 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = world * nx * ny * nz * args.steps / (ms * 1e-3) / 1e9   # every rank's volume per step, all ranks
+    value = nx * ny * nz * args.steps / (ms * 1e-3) / 1e9   # one volume per step across all ranks
     assert int(res["hist"].sum().item()) == nx * ny * nz     # the all-reduced histogram covers every voxel
 
     # roofline of the dominant kernel (the fused pass), this rank's slab
@@ -236,64 +245,44 @@ def main():
         except Exception:
             traffic = None
 
-    # ---- e2e: the reference-facing drop-in calls on a pageable host Volume (the headline
-    # e2e), and the host-buffer session on a pinned volume (side key)
+    # ---- N > 1 side measurements: every rank reduces its OWN c2 volume (replicas: weak, no
+    # data-path collective), and config 3 (one 16 GiB u16 volume) z-slab sharded
+    replicas = c3_zslab = None
+    if world > 1:
+        sh.close()
+        del slab, sh
+        torch.cuda.empty_cache()
+        replicas = bench_replicas(args, spec, schemes, level_of, plan, device, rank, world, dist)
+        if not args.no_configs:
+            c3_zslab = bench_c3_zslab(device, rank, world, dist)
+
+    # ---- e2e: the reference-facing drop-in calls on a pageable host Volume (N > 1: one volume
+    # per rank), and the host-buffer session on a pinned volume (side key)
+    full = synth.generate(synth.config("c2", seed=rank if world > 1 else 0), device=device) if world > 1 else slab
     e2e = e2e_session = None
     if not args.no_e2e:
-        host_np = slab.cpu().numpy()
+        host_np = full.cpu().numpy()
         e2e = bench_e2e_dropin(host_np, device, world, dist)
-        e2e_session = bench_e2e_session(slab, spec, schemes, device, world, dist)
+        e2e_session = bench_e2e_session(full, spec, schemes, device, world, dist)
+        e2e["interactive_builder"] = bench_e2e_interactive(host_np, device, world, dist)
         del host_np
-
-    # ---- N > 1: ONE c2 volume z-slab sharded across the ranks (strong scaling): LUT broadcast
-    # from the top-slab owner, fused pass per slab storing its atlas rows into rank 0's atlases
-    # over NVLink (CUDA IPC), histogram all-reduce -- SURVEY s8(e)
-    zslab = None
-    if world > 1:
-        del slab
-        torch.cuda.empty_cache()
-        shz = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), rank, world,
-                             device, peer_atlases=True)
-        zs = synth.generate(spec, z_range=(shz.z0, shz.z1), device=device)
-        for _ in range(max(3, args.warmup // 4)):
-            shz.step(zs)
-        zsteps = max(10, min(args.steps, 100))
-        torch.cuda.synchronize()
-        dist.barrier()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(zsteps):
-            rz = shz.step(zs)
-        a1.record()
-        torch.cuda.synchronize()
-        zt = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=device)
-        dist.all_reduce(zt, op=dist.ReduceOp.MAX)
-        zms = float(zt.item()) / zsteps
-        assert int(rz["hist"].sum().item()) == nx * ny * nz
-        zslab = {"workload": "c2 (one 1024^3 volume) z-slab sharded across the ranks", "scaling": "strong",
-                 "ms_per_step": zms, "gvoxel_per_s": nx * ny * nz / zms / 1e6, "slab": [shz.z0, shz.z1],
-                 "collectives": "LUT broadcast (NCCL), histogram all-reduce (NCCL), atlas rows stored into rank 0's "
-                                "atlases by the fused kernels over NVLink (CUDA IPC)"}
-        shz.close()
-        del zs, shz
-        torch.cuda.empty_cache()
-        slab = synth.generate(synth.config("c2", seed=rank), device=device)
 
     # ---- CPU baseline (rank 0, N=1 only): ctprev's own functions (baseline/_ref; the oracle
     # port when absent) fanned out over all host cores on 512 slices of this volume
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import bench_ref
-        cpu = bench_ref.cpu_baseline(slab.cpu().numpy(), 512)
+        cpu = bench_ref.cpu_baseline(full.cpu().numpy(), 512)
+    slab = full
 
     mip = None
     if not args.no_mip:
         del slab
         torch.cuda.empty_cache()
-        mip = bench_mip(args, device, rank, world, dist)
+        mip = bench_mip(args, device, rank, world, dist, mode="tiles" if world > 1 else "single")
         if world > 1:
-            mip["sort_last"] = bench_mip(args, device, rank, world, dist, sort_last=True)
+            mip["sort_last"] = bench_mip(args, device, rank, world, dist, mode="sort_last")
+            mip["replicas"] = bench_mip(args, device, rank, world, dist, mode="replicas")
     others = None
     if not args.no_configs and world == 1:
         torch.cuda.empty_cache()
@@ -302,17 +291,15 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GVoxel/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded config-2 generator, on device)",
-            "config": {"workload": "c2: 1024^3 u8, hist + artifact-bin filter + 512/256/128 levels + slicemap "
-                                   "atlases (8x4096^2, 4x2048^2, 2x1024^2)",
-                       "voxels_per_step": world * nx * ny * nz,
-                       "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (one c2 scan per GPU)",
-                       "l2": "input 1 GiB per step > 126 MB L2 (no flush needed)"},
+            "config": bench_ref.headline_config(world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "kernel": "preview_kernel<uint8_t,3,1024 thr>: the whole step in one cooperative launch "
-                                   "(artifact-LUT phase + fused hist/filter/pyramid/atlas pass)", "kernel_ms": kmean,
+                         "kernel": ("preview_kernel<uint8_t,3,1024 thr>: the whole step in one cooperative launch "
+                                    "(artifact-LUT phase + fused hist/filter/pyramid/atlas pass)") if world == 1 else
+                                   ("preview_kernel<uint8_t,3,1024 thr> on this rank's z-slab (fused hist/filter/"
+                                    "pyramid/atlas pass, atlas rows stored into rank 0's atlases)"), "kernel_ms": kmean,
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -320,7 +307,8 @@ def main():
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "mip": mip,
-            "c2_zslab": zslab,
+            "replicas": replicas,
+            "c3_zslab": c3_zslab,
             "other_configs": others,
         }
         print(json.dumps(line))
@@ -402,6 +390,121 @@ def bench_e2e_dropin(vol_np, device, world, dist, steps: int = 8, warmup: int = 
             uninstall()
 
 
+def bench_e2e_interactive(vol_np, device, world, dist, steps: int = 3):
+    """Side key of e2e: ctprev's own ``build_interactive_preview`` (pipeline.py:267-309) after
+    install() on the pageable 1 GiB host Volume -- one upload, the three scheme levels from ONE
+    fused pass, circle mask / histograms / atlases on the device, ctprev's own circle detector
+    and Otsu on the host; the device cache is cleared every step."""
+    import torch
+    from paper_2311_15038_b200 import hostio, ops
+    uninstall = None
+    fn, how = ops.build_interactive_preview, "paper_2311_15038_b200.build_interactive_preview"
+    try:
+        ref_dir = ROOT / "baseline" / "_ref"
+        if ref_dir.is_dir() and str(ref_dir) not in sys.path:
+            sys.path.insert(0, str(ref_dir))
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ctp_ref_numba_cache")
+        import ctprev.pipeline
+        from paper_2311_15038_b200.install import install, uninstall
+        install()
+        fn, how = ctprev.pipeline.build_interactive_preview, "ctprev.pipeline.build_interactive_preview after install()"
+    except Exception:  # pragma: no cover - depends on the box
+        pass
+    try:
+        from paper_2311_15038_b200.types import FACTORY
+        v = FACTORY.Volume(vol_np)
+        hostio.CACHE.clear()
+        fn(v)  # warm-up (numba / scipy imports of the host helpers)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(steps):
+            hostio.CACHE.clear()
+            t0 = time.perf_counter()
+            ip = fn(v)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        nz, ny, nx = vol_np.shape
+        return {"ms_per_volume": min(ts) * 1e3, "gvoxel_per_s": nz * ny * nx / min(ts) / 1e9, "path": how,
+                "warnings": list(ip.warnings), "thresholds": {str(k): t for k, t in ip.thresholds.items()}}
+    except Exception as e:  # pragma: no cover - reported in the line
+        return {"error": repr(e)[:200]}
+    finally:
+        if uninstall is not None:
+            uninstall()
+
+
+def bench_replicas(args, spec, schemes, level_of, plan, device, rank, world, dist):
+    """N > 1 side key: every rank reduces its OWN c2 volume (no data-path collective)."""
+    import torch
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.dist import DeviceSlabCompute, ShardedPreview
+    nz, ny, nx = spec.shape
+    sh = ShardedPreview(spec.shape, schemes, level_of, DeviceSlabCompute(torch.uint8, plan.fused), 0, 1, device)
+    vol = synth.generate(synth.config("c2", seed=rank), device=device)
+    for _ in range(max(3, args.warmup)):
+        sh.step(vol)
+    steps = max(10, min(args.steps, 200))
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(steps):
+        sh.step(vol)
+    a1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    del vol, sh
+    torch.cuda.empty_cache()
+    return {"workload": f"c2, one 1024^3 volume per rank x{world} (no data-path collective)", "scaling": "weak",
+            "ms_per_step": ms, "gvoxel_per_s": world * nx * ny * nz / ms / 1e6}
+
+
+def bench_c3_zslab(device, rank, world, dist, steps: int = 5):
+    """N > 1 side key: config 3 (ONE 2048^3 12-bit u16 volume, 16 GiB) z-slab sharded: LUT from the
+    top-slab owner, 4-level fused pass per slab storing into rank 0's atlases (peer mapping),
+    4096-bin histogram all-reduce -- BASELINE config 3 at 1/2/4/8 GPUs."""
+    import torch
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.device import AtlasSpec
+    from paper_2311_15038_b200.dist import DeviceSlabCompute, ShardedPreview
+    from paper_2311_15038_b200.pipeline import plan_preview
+    from paper_2311_15038_b200.types import plan_scheme
+    spec = synth.config("c3")
+    nz, ny, nx = spec.shape
+    schemes = {1024: AtlasSpec(1024, 4096, 4, 64), 512: AtlasSpec.of(plan_scheme(512)),
+               256: AtlasSpec.of(plan_scheme(256)), 128: AtlasSpec.of(plan_scheme(128))}
+    plan = plan_preview(spec.shape, schemes)
+    sh = ShardedPreview(spec.shape, schemes, dict(plan.scheme_level), DeviceSlabCompute(torch.uint16, plan.fused),
+                        rank, world, device, peer_atlases=True)
+    slab = synth.generate(spec, z_range=(sh.z0, sh.z1), device=device)
+    for _ in range(2):
+        sh.step(slab)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(steps):
+        r = sh.step(slab)
+    a1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    assert int(r["hist"].sum().item()) == nx * ny * nz
+    sh.close()
+    del slab, sh
+    torch.cuda.empty_cache()
+    return {"workload": "c3: one 2048^3 12-bit u16 volume (16 GiB) z-slab sharded, 4096-bin hist + filter o rescale "
+                        "+ 4 levels + atlases", "scaling": "strong", "ms_per_step": ms,
+            "gvoxel_per_s": nx * ny * nz / ms / 1e6,
+            "collectives": "LUT all-reduce from the top-slab owner, histogram all-reduce (NCCL), atlas rows stored "
+                           "into rank 0's atlases by the fused kernels (CUDA IPC peer mapping)"}
+
+
 def bench_e2e_session(slab, spec, schemes, device, world, dist):
     """Side key: the host-buffer session (pinned volume in, pinned atlases out, z-chunks
     streamed on three CUDA streams) -- this package's own streaming API."""
@@ -449,23 +552,28 @@ def bench_e2e_session(slab, spec, schemes, device, world, dist):
     return out
 
 
-def bench_mip(args, device, rank, world, dist, sort_last: bool = False):
-    """Config 4: 36 MIP azimuths, 1024^2 RGBA8.  Default: every GPU renders the
-    turntable of its own volume (N > 1: replicas, weak).  ``sort_last``: ONE
-    volume z-slab sharded across the ranks, each rank rendering its row band from
-    its slab + halo and storing it into rank 0's images over NVLink (strong)."""
+def bench_mip(args, device, rank, world, dist, mode: str = "single"):
+    """Config 4: 36 MIP azimuths, 1024^2 RGBA8, one turntable per batch.
+      single    : N = 1, the whole volume on the GPU
+      tiles     : N > 1, the volume REPLICATED on every rank, the image rows split evenly (each
+                  rank's band stored into rank 0's images over NVLink by its render kernel) --
+                  BASELINE config 4's image-tile split (strong)
+      sort_last : N > 1, ONE volume z-slab sharded, each rank rendering the row band of its
+                  slab + halo into rank 0's images (strong)
+      replicas  : N > 1, every rank renders the turntable of its own volume (weak)"""
     import math
     import torch
     from paper_2311_15038_b200 import synth
     from paper_2311_15038_b200.dist import DeviceRenderCompute, ShardedRender
     from paper_2311_15038_b200.types import ViewParams
-    spec = synth.config("c4", seed=0 if sort_last else rank)
+    spec = synth.config("c4", seed=rank if mode == "replicas" else 0)
     n = spec.shape[0]
     dim = 1024
     steps = math.ceil(4 * math.sqrt(3.0) / 2.0 * n)  # 0.5-voxel step over the 2R window: 3548 for 1024^3
     views = [ViewParams(azimuth_deg=10.0 * k, image_dim=dim, steps=steps, mode="mip") for k in range(36)]
-    if sort_last:
-        sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True)
+    if mode in ("tiles", "sort_last"):
+        sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), rank, world, device, peer_images=True,
+                           replicated=mode == "tiles")
     else:
         sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), 0, 1, device)
     local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
@@ -485,24 +593,24 @@ def bench_mip(args, device, rank, world, dist, sort_last: bool = False):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    frames = 36 * args.mip_batches * (1 if sort_last else world)
+    frames = 36 * args.mip_batches * (world if mode == "replicas" else 1)
     del local
     sr.close()
     from paper_2311_15038_b200 import device as dev
     dev.render_release()
     torch.cuda.empty_cache()
+    how = {"single": "", "tiles": f"; volume replicated x{world}, image rows split, bands stored into rank 0's "
+                                  "images over NVLink by the render kernels",
+           "sort_last": f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's images over "
+                        "NVLink by the render kernels", "replicas": f"; replicas x{world} (one volume per GPU)"}[mode]
     return {"value": frames / (ms * 1e-3), "unit": "frames/s", "ms_per_frame": ms / frames,
             "gsamples_per_s": frames * dim * dim * steps / (ms * 1e-3) / 1e9, "steps_per_ray": steps,
             "image": "1024^2 RGBA8", "volume": "1024^3 u8 (config-4 generator)", "views_per_batch": 36,
             "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
-            "bound": "texture pipe: one tld4 gather per sample; ncu l1tex data-pipe TEX wavefronts 76% of peak, "
-                     "L1 hit 92% (profiles/r01_render_c4_mip_ncu.txt)",
-            "scaling": "strong" if sort_last else "weak",
-            "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + (
-                f"; z-slab x{world} sort-last: row bands from slab + halo, stored into rank 0's images over "
-                "NVLink by the render kernels" if sort_last else ("" if world == 1 else
-                                                                  f"; replicas x{world} (one volume per GPU)"))}
+            "bound": "texture pipe: one tld4 gather per sample (ncu: profiles/r01_render_c4_mip_ncu.txt)",
+            "scaling": "weak" if mode == "replicas" else "strong", "mode": mode,
+            "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + how}
 
 
 def _time_steps(fn, reps: int, warmup: int = 2):
