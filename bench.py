@@ -46,6 +46,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+CLOCK_WARMUP_S = 0.5
 METRIC = "pipeline GVoxel/s (hist+filter+slicemaps) & MIP frames/s, % of HBM roofline"
 SCHEMES = (512, 256, 128)
 
@@ -199,6 +200,15 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    # plus untimed steps for CLOCK_WARMUP_S so the SM clocks have left their idle state (a 20-step
+    # timed region is ~5 ms).  N > 1: a fixed count (the steps' collectives pair the ranks' steps)
+    n_clock = 0
+    t_w = time.perf_counter()
+    while (n_clock < 2000) if world > 1 else (n_clock % 64 or time.perf_counter() - t_w < CLOCK_WARMUP_S):
+        step()
+        n_clock += 1
+        if n_clock % 64 == 0:
+            torch.cuda.synchronize()
     sh.fused_events = None
     torch.cuda.synchronize()
     if world > 1:
@@ -305,6 +315,7 @@ def main():
             "e2e": e2e,
             "e2e_session": e2e_session,
             "gpu_launches": launches,
+            "clock_warmup_steps": n_clock,
             "clocks": sampler.summary(),
             "mip": mip,
             "replicas": replicas,
@@ -578,6 +589,11 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
         sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), 0, 1, device)
     local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
     sr.render(local, views, channels=4, fp32=True)   # warmup (row planes allocated once)
+    if world == 1:
+        _warm_clocks(lambda: sr.render(local, views, channels=4, fp32=True))
+    else:  # every rank renders the same number of warm-up batches (the batches synchronise the ranks)
+        for _ in range(8):
+            sr.render(local, views, channels=4, fp32=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -613,10 +629,21 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + how}
 
 
+def _warm_clocks(fn, seconds: float = 0.5):
+    """Run ``fn`` back to back for ``seconds``: SM clocks drop while the GPU idles (e.g. during
+    a host-side leg), and a side measurement of a few ms would otherwise time the ramp."""
+    import torch
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        fn()
+        torch.cuda.synchronize()
+
+
 def _time_steps(fn, reps: int, warmup: int = 2):
     import torch
     for _ in range(warmup):
         fn()
+    _warm_clocks(fn)
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
@@ -737,6 +764,7 @@ def bench_other_configs(device):
         ps = PreviewStream(spec.shape, torch.uint16, device=device)
         for _ in range(3):
             ps.process(vol)
+        _warm_clocks(lambda: ps.process(vol))
         reps = []
         for _ in range(10):  # per-volume times with a phase breakdown (CUDA events between phases)
             ps.trace = []

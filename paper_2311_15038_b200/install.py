@@ -57,6 +57,11 @@ def install(package: str = "ctprev", exclude=()) -> list[str]:
     FACTORY.InteractivePreview = pl.InteractivePreview
     FACTORY.ListPreview = pl.ListPreview
     FACTORY.Circle = importlib.import_module(f"{package}.mask").Circle
+    # the error classes must BE the reference's (its callers catch them, pipeline.py:176-191,
+    # cli.py:211; our builders catch NoCircleFound / DegenerateHistogram raised by the
+    # reference's host helpers): rebind them when ctprev was imported after this package
+    from . import errors as _errors
+    _errors.bind(importlib.import_module(f"{package}.errors"))
     patched = []
     for name, mods in BINDINGS.items():
         if name in exclude:

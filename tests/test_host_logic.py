@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import importlib
 import math
+import os
 import re
 import sys
 from pathlib import Path
@@ -170,3 +171,29 @@ def test_reference_arm_is_independent_of_the_package():
                 sp.thickness, sp.speckle_p) == (p["shape"], p["seed"], p["n_shells"], p["bg"], p["shell"], p["axes"],
                                                 p["thickness"], p["speckle_p"]), name
         assert [tuple(s) for s in sp.shells()] == [tuple(s) for s in bench_ref.shells(p)], name
+
+
+def test_install_binds_reference_error_classes_when_imported_later():
+    """ctprev imported AFTER this package: install() rebinds the error classes everywhere in
+    the package, so the drop-in builders catch ctprev's own NoCircleFound / DegenerateHistogram
+    (raised by its host circle detector / Otsu) and raise what ctprev's callers catch."""
+    import subprocess
+    ref = next((d for d in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")) if (d / "ctprev").is_dir()),
+               None)
+    if ref is None:
+        pytest.skip("ctprev not installed nor mounted")
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2311_15038_b200 as P\n"
+            "from paper_2311_15038_b200 import errors, ingest, ops, types\n"
+            "assert not errors.FROM_REFERENCE\n"
+            "sys.path.insert(0, %r)\n"
+            "import ctprev.errors as E\n"
+            "P.install()\n"
+            "assert ops.RangeOutOfBounds is E.RangeOutOfBounds and ingest.MissingSlice is E.MissingSlice\n"
+            "assert types.DimensionMismatch is E.DimensionMismatch and P.NoCircleFound is E.NoCircleFound\n"
+            "from paper_2311_15038_b200.errors import NoCircleFound\n"
+            "assert NoCircleFound is E.NoCircleFound\n"
+            "print('ok')\n") % (str(ROOT), str(ref))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                       env={**os.environ, "NUMBA_CACHE_DIR": "/tmp/ctp_numba_err_test"})
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr

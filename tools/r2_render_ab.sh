@@ -1,0 +1,7 @@
+for rep in 1 2; do
+for lib in default variants/libr1.so; do
+  arg=""; [ "$lib" != default ] && arg="--lib $lib"
+  python tools/prof_render.py $arg --mode mip --batches 2 | sed "s|^|$lib |"
+  python tools/prof_render.py $arg --mode alpha --batches 2 | sed "s|^|$lib |"
+done
+done
