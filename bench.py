@@ -281,8 +281,7 @@ def main():
     # port when absent) fanned out over all host cores on 512 slices of this volume
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import bench_ref
-        cpu = bench_ref.cpu_baseline(full.cpu().numpy(), 512)
+        cpu = cpu_baseline_subprocess(full)
     slab = full
 
     mip = None
@@ -326,6 +325,27 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def cpu_baseline_subprocess(vol_t) -> dict:
+    """bench_ref.cpu_baseline on this volume in a separate, CUDA-free python process (the
+    volume handed over through /dev/shm): forking the benchmark process itself -- which holds
+    a CUDA context and pinned host buffers -- left the later GPU measurements 2-3x slower."""
+    import tempfile
+    import numpy as np
+    d = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.NamedTemporaryFile(suffix=".npy", dir=d, delete=False) as f:
+        path = f.name
+    try:
+        np.save(path, vol_t.cpu().numpy())
+        code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import bench_ref; "
+                "print(json.dumps(bench_ref.cpu_baseline(np.load(%r), 512)))") % (str(ROOT), path)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900)
+        if r.returncode != 0:
+            return {"error": r.stderr.strip().splitlines()[-1][:200] if r.stderr.strip() else f"rc {r.returncode}"}
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    finally:
+        os.unlink(path)
 
 
 def bench_e2e_dropin(vol_np, device, world, dist, steps: int = 8, warmup: int = 2):

@@ -16,3 +16,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:prev
   python tools/prof_preview.py --config c3 --schemes 1024,512,256,128 --reps 2 > $OUT/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:^(?!synth)' -c 40 -o $OUT/secondary -f \
   python tools/prof_secondary.py > $OUT/ncu_secondary.log 2>&1; echo "ncu secondary rc=$?"
+# summarise on the box (ncu is there) and keep the returned directory small
+python tools/summarise_r02.py --tag r02 > $OUT/summary.log 2>&1; echo "summary rc=$?"
+mkdir -p $OUT/profiles && cp profiles/r02_* profiles/traffic_fused_c2.json $OUT/profiles/ 2>/dev/null
+du -sh $OUT/*.ncu-rep
+rm -f $OUT/*.ncu-rep  # 35-80 MB each: over the 64 MiB return limit (the summaries carry the numbers)
