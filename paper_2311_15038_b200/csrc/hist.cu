@@ -216,6 +216,36 @@ __global__ void __launch_bounds__(kHistThreads) lut_apply_u16_kernel(const uint1
     }
 }
 
+// The same over 16-byte vectors (8 voxels: one 16-byte load, one 8-byte store per
+// thread and vector) for the aligned bulk of the array; the scalar kernel above
+// takes the tail.
+__global__ void __launch_bounds__(kHistThreads) lut_apply_u16_vec_kernel(const uint4* __restrict__ in,
+                                                                         uint2* __restrict__ out, int64_t nv,
+                                                                         const uint8_t* __restrict__ lut,
+                                                                         unsigned long long* __restrict__ hist) {
+  __shared__ uint32_t hs[4096];
+  for (int i = threadIdx.x; i < 4096; i += kHistThreads) hs[i] = lut[i];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * kHistThreads + threadIdx.x; i < nv; i += (int64_t)gridDim.x * kHistThreads) {
+    const uint4 q = __ldcs(in + i);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      o[2 * k] = atomicAdd(&hs[min(w[k] & 0xFFFFu, 4095u)], kCountOne);
+      o[2 * k + 1] = atomicAdd(&hs[min(w[k] >> 16, 4095u)], kCountOne);
+    }
+    out[i] = make_uint2(__byte_perm(__byte_perm(o[0], o[1], 0x0040), __byte_perm(o[2], o[3], 0x0040), 0x5410),
+                        __byte_perm(__byte_perm(o[4], o[5], 0x0040), __byte_perm(o[6], o[7], 0x0040), 0x5410));
+  }
+  __syncthreads();
+  if (hist)
+    for (int b = threadIdx.x; b < 4096; b += kHistThreads) {
+      const uint32_t c = hs[b] >> 12;
+      if (c) atomicAdd(hist + b, (unsigned long long)c);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One launch for the whole artifact-LUT step (mask.py:215-231 + 241-245):
 // every CTA histograms a share of the top slab in shared memory and adds it to
@@ -376,10 +406,22 @@ int ctp_lut_apply_u16(const uint16_t* in, uint8_t* out, int64_t n, const uint8_t
   CTP_REQUIRE(in && out && lut4096, CTP_E_INVALID, "ctp_lut_apply_u16: null pointer");
   CTP_REQUIRE(n >= 0, CTP_E_INVALID, "negative length");
   if (n == 0) return CTP_OK;
-  int grid = grid_for(n, kHistThreads, 8);
-  while ((n + (int64_t)grid - 1) / grid >= (1LL << 20) - 1) grid *= 2;  // a block's share fits the count field
-  lut_apply_u16_kernel<<<grid, kHistThreads, 0, as_stream(stream)>>>(in, out, n, lut4096,
-                                                                      reinterpret_cast<unsigned long long*>(hist4096));
+  auto* h = reinterpret_cast<unsigned long long*>(hist4096);
+  int64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0 && n >= 8) {
+    const int64_t nv = n / 8;
+    int grid = grid_for(nv, kHistThreads, 8);
+    while ((nv * 8 + (int64_t)grid - 1) / grid >= (1LL << 20) - 1) grid *= 2;  // a block's share fits the count field
+    lut_apply_u16_vec_kernel<<<grid, kHistThreads, 0, as_stream(stream)>>>(reinterpret_cast<const uint4*>(in),
+                                                                          reinterpret_cast<uint2*>(out), nv, lut4096, h);
+    CTP_CUDA_CHECK_LAUNCH("lut_apply_u16_vec_kernel");
+    done = nv * 8;
+  }
+  if (done == n) return CTP_OK;
+  const int64_t rest = n - done;
+  int grid = grid_for(rest, kHistThreads, 8);
+  while ((rest + (int64_t)grid - 1) / grid >= (1LL << 20) - 1) grid *= 2;  // a block's share fits the count field
+  lut_apply_u16_kernel<<<grid, kHistThreads, 0, as_stream(stream)>>>(in + done, out + done, rest, lut4096, h);
   CTP_CUDA_CHECK_LAUNCH("lut_apply_u16_kernel");
   return CTP_OK;
 }

@@ -308,22 +308,33 @@ __global__ void __launch_bounds__(256) encode_atlas_kernel(const uint8_t* __rest
   }
 }
 
-// One CTA per cube row (slice k, row y): s bytes gathered from the atlas cell row.
+// One CTA per ATLAS row (map m, row R), the inverse of encode_atlas_kernel: every
+// 16-byte chunk of the atlas row is one slice row segment (slice k = m*grid^2 +
+// (R / s)*grid + C / s, row R % s, columns C % s ..) copied with one 16-byte load
+// and store; cells past the last slice (k >= s) are skipped.  (A CTA per cube row
+// left 7/8 of its threads idle for s = 512: 12% of HBM.)  Byte path when s or the
+// atlas rows are not 16-byte granular.
 __global__ void __launch_bounds__(256) decode_atlas_kernel(const uint8_t* __restrict__ atlases, int s, int grid,
                                                            int atlas_dim, uint8_t* __restrict__ cube) {
-  const int64_t r = blockIdx.x;  // k * s + y
-  const int64_t k = r / s;
-  const int y = (int)(r - k * s);
-  const int64_t per = (int64_t)grid * grid;
-  const int64_t m = k / per, w = k - m * per;
-  const int cy = (int)(w / grid), cx = (int)(w - (w / grid) * grid);
-  const uint8_t* src = atlases + m * (int64_t)atlas_dim * atlas_dim + (int64_t)(cy * s + y) * atlas_dim + cx * s;
-  uint8_t* dst = cube + r * s;
+  const int64_t row = blockIdx.x;  // m * atlas_dim + R
+  const int64_t m = row / atlas_dim;
+  const int R = (int)(row - m * atlas_dim);
+  const int cy = R / s, y = R - cy * s;
+  const int64_t k0 = m * (int64_t)grid * grid + (int64_t)cy * grid;  // slice of cell (cy, 0)
+  const uint8_t* src = atlases + row * atlas_dim;
   if (s % 16 == 0 && atlas_dim % 16 == 0) {
-    for (int x = threadIdx.x * 16; x < s; x += blockDim.x * 16)
-      *reinterpret_cast<uint4*>(dst + x) = __ldg(reinterpret_cast<const uint4*>(src + x));
+    for (int C = threadIdx.x * 16; C < atlas_dim; C += blockDim.x * 16) {
+      const int cx = C / s, x = C - cx * s;
+      const int64_t k = k0 + cx;
+      if (k < s)
+        *reinterpret_cast<uint4*>(cube + (k * s + y) * s + x) = __ldg(reinterpret_cast<const uint4*>(src + C));
+    }
   } else {
-    for (int x = threadIdx.x; x < s; x += blockDim.x) dst[x] = __ldg(src + x);
+    for (int C = threadIdx.x; C < atlas_dim; C += blockDim.x) {
+      const int cx = C / s, x = C - cx * s;
+      const int64_t k = k0 + cx;
+      if (k < s) cube[(k * s + y) * s + x] = __ldg(src + C);
+    }
   }
 }
 
@@ -340,6 +351,7 @@ __device__ __forceinline__ bool in_circle(int64_t x, int64_t y, double cx, doubl
 // the integers around the one nearest cx and fails beyond two boundaries,
 // found by binary search with the exact predicate (row_span_kernel, one thread
 // per row y); every slice then applies the same spans with 16-byte copies.
+
 __global__ void circle_span_kernel(int64_t ny, int64_t nx, double cx, double cy, double r2, int2* __restrict__ span) {
   const int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (y >= ny) return;
@@ -529,7 +541,8 @@ int ctp_decode_atlas_u8(const uint8_t* atlases, int32_t s, int32_t grid, int32_t
   ctp_level_out lo{const_cast<uint8_t*>(atlases), CTP_LAYOUT_ATLAS, s, grid, atlas_dim, map_count, 0};
   int rc = check_level_desc(lo, s, s, s, 0);
   if (rc != CTP_OK) return rc;
-  const int64_t rows = (int64_t)s * s;
+  const int64_t rows = (int64_t)atlas_dim * map_count;
+  CTP_REQUIRE(rows < (1LL << 31), CTP_E_INVALID, "ctp_decode_atlas_u8: too many atlas rows");
   decode_atlas_kernel<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(atlases, s, grid, atlas_dim, cube);
   CTP_CUDA_CHECK_LAUNCH("decode_atlas_kernel");
   return CTP_OK;
