@@ -378,22 +378,31 @@ def bench_e2e_dropin(vol_np, device, world, dist, steps: int = 8, warmup: int = 
         v = FACTORY.Volume(vol_np)
         nz, ny, nx = vol_np.shape
         sizes = {}
+        calls = {}
 
-        def step():
+        def step(trace: bool = False):
+            def t(name, fn):
+                if not trace:
+                    return fn()
+                c0 = time.perf_counter()
+                r = fn()
+                calls[name] = round((time.perf_counter() - c0) * 1e3, 3)
+                return r
             hostio.CACHE.clear()
-            h = api.volume_histogram(v)                                   # volume.py:252-262
-            bins = api.artifact_bins(v)                                   # mask.py:215-231
-            f = api.filter_histogram_bins(v, bins)                        # mask.py:234-246
+            h = t("volume_histogram", lambda: api.volume_histogram(v))                 # volume.py:252-262
+            bins = t("artifact_bins", lambda: api.artifact_bins(v))                     # mask.py:215-231
+            f = t("filter_histogram_bins", lambda: api.filter_histogram_bins(v, bins))  # mask.py:234-246
             out = [h.bins.nbytes, f.voxels.nbytes]
             for s in SCHEMES:
-                lv = api.downscale_volume(f, (s, s, s))                   # volume.py:277-309
-                sm = api.encode_slicemaps(lv, s)                          # slicemap.py:120-142
+                lv = t(f"downscale_volume_{s}", lambda: api.downscale_volume(f, (s, s, s)))  # volume.py:277-309
+                sm = t(f"encode_slicemaps_{s}", lambda: api.encode_slicemaps(lv, s))       # slicemap.py:120-142
                 out += [lv.voxels.nbytes, sum(a.nbytes for a in sm.atlases)]
             sizes["d2h"] = sum(out)
             return h
 
         for _ in range(warmup):
             step()
+        step(trace=True)  # per-call wall times of one untimed step
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -413,6 +422,7 @@ def bench_e2e_dropin(vol_np, device, world, dist, steps: int = 8, warmup: int = 
         return {"value": world * nz * ny * nx * steps / sec / 1e9, "unit": "GVoxel/s",
                 "h2d_bytes_per_step": nz * ny * nx + 3 * ny * nx + 256, "d2h_bytes_per_step": sizes["d2h"],
                 "steps": steps, "ms_per_step": sec / steps * 1e3, "gpu_launches_per_step": launches / steps,
+                "calls_ms": calls,
                 "path": how + ": volume_histogram, artifact_bins, filter_histogram_bins, downscale_volume x3, "
                         "encode_slicemaps x3 on a pageable 1 GiB Volume; fresh host arrays out; device cache "
                         "cleared every step" + ("" if world == 1 else f"; one volume per rank x{world}")}
