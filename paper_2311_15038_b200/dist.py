@@ -25,6 +25,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import trace
 from .device import AtlasSpec
 
 
@@ -212,27 +213,31 @@ class ShardedPreview:
         else:
             lut = torch.zeros(self.compute.nbins, dtype=torch.uint8, device=self.device)
         if self.world > 1:
-            if self.peer:
-                # peer mode: every rank's pass stores into rank 0's atlases, which are reused by
-                # every step -- so the LUT is distributed by an all-reduce (MAX over the owner's
-                # LUT and zeros) instead of a broadcast: no rank can start its pass before rank 0
-                # has entered this step, i.e. finished with the previous step's atlases
-                dist.all_reduce(lut, op=dist.ReduceOp.MAX, group=self.group)
-            else:
-                dist.broadcast(lut, src=owner, group=self.group)
+            with trace.range("sharded.lut_exchange"):
+                if self.peer:
+                    # peer mode: every rank's pass stores into rank 0's atlases, which are reused by
+                    # every step -- so the LUT is distributed by an all-reduce (MAX over the owner's
+                    # LUT and zeros) instead of a broadcast: no rank can start its pass before rank 0
+                    # has entered this step, i.e. finished with the previous step's atlases
+                    dist.all_reduce(lut, op=dist.ReduceOp.MAX, group=self.group)
+                else:
+                    dist.broadcast(lut, src=owner, group=self.group)
         if not zeroed:
             self.hist.zero_()
         if self.fused_events is not None:
             self.fused_events[0].record()
-        self.compute.fused(slab, lut, self.z0, nz, self.hist, self.atlases)
+        with trace.range("sharded.fused_pass"):
+            self.compute.fused(slab, lut, self.z0, nz, self.hist, self.atlases)
         if self.fused_events is not None:
             self.fused_events[1].record()
         if self.world > 1:
             # stream-ordered after every rank's pass: when rank 0's all-reduce completes, every
             # rank's kernel -- and, in peer mode, its stores into rank 0's atlases -- is done
-            dist.all_reduce(self.hist, group=self.group)
+            with trace.range("sharded.hist_allreduce"):
+                dist.all_reduce(self.hist, group=self.group)
             if gather and not self.peer:
-                self._gather()
+                with trace.range("sharded.atlas_gather"):
+                    self._gather()
         return {"hist": self.hist, "lut": lut, "atlases": self.atlases}
 
     def close(self) -> None:

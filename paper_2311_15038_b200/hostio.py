@@ -32,6 +32,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 import torch
 
+from . import trace
+
 _NP2T = {np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.uint16, np.dtype(np.int64): torch.int64,
          np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64, np.dtype(np.int32): torch.int32}
 
@@ -135,6 +137,11 @@ def _stager(device) -> _Stager:
 
 def h2d(arr: np.ndarray, device) -> torch.Tensor:
     """A device copy of a host array, ordered before later work on the current stream."""
+    with trace.range("hostio.h2d"):
+        return _h2d(arr, device)
+
+
+def _h2d(arr: np.ndarray, device) -> torch.Tensor:
     a = np.ascontiguousarray(arr)
     dt = _NP2T.get(a.dtype)
     if dt is None:
@@ -189,6 +196,11 @@ def d2h(t: torch.Tensor) -> np.ndarray:
     memory, which the returned array keeps alive."""
     if t.numel() * t.element_size() < PINNED_OUT_MIN_BYTES:
         return t.cpu().numpy()
+    with trace.range("hostio.d2h"):
+        return _d2h_pinned(t)
+
+
+def _d2h_pinned(t: torch.Tensor) -> np.ndarray:
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     h.copy_(t, non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()

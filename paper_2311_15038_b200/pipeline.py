@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import device as dev
+from . import trace
 from .device import AtlasSpec
 
 
@@ -107,12 +108,14 @@ def run_preview(vol: torch.Tensor, plan: PreviewPlan, n_top: int = 3, frac: floa
     nz, ny, nx = vol.shape
     if nx % (16 // vol.element_size()) and set(plan.fused) == {0}:
         # rows not 16-byte vectorisable: filter (+ rescale) + histogram with the any-size LUT kernels
-        lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
-        apply = dev.lut_apply_u8 if vol.dtype == torch.uint8 else dev.lut_apply_u16
-        outs = {0: apply(vol, lut, hist=hist)}
+        with trace.range("preview.lut_apply"):
+            lut, flags = dev.artifact_lut_fused(vol, n_top, frac, zero_hist=hist)
+            apply = dev.lut_apply_u8 if vol.dtype == torch.uint8 else dev.lut_apply_u16
+            outs = {0: apply(vol, lut, hist=hist)}
     else:
         # the whole step (artifact LUT + fused pass) in one cooperative launch
-        outs, hist, lut, flags = dev.preview_step(vol, plan.fused, n_top, frac, hist=hist)
+        with trace.range("preview.fused_step"):
+            outs, hist, lut, flags = dev.preview_step(vol, plan.fused, n_top, frac, hist=hist)
     atlases, levels = {}, {}
     filtered = outs.get(0) if plan.fused.get(0) == "xyz" else None
     for s, l in plan.scheme_level.items():
@@ -120,9 +123,10 @@ def run_preview(vol: torch.Tensor, plan: PreviewPlan, n_top: int = 3, frac: floa
             atlases[s] = outs[l]
     for s in plan.general:
         spec = plan.schemes[s]
-        lv = dev.downscale(filtered, (min(s, nx), min(s, ny), min(s, nz)))
-        levels[s] = lv
-        atlases[s] = dev.encode_atlas(lv, spec)
+        with trace.range(f"preview.general_level_{s}"):
+            lv = dev.downscale(filtered, (min(s, nx), min(s, ny), min(s, nz)))
+            levels[s] = lv
+            atlases[s] = dev.encode_atlas(lv, spec)
     return DevicePreview(hist, lut, flags, atlases, levels, filtered)
 
 

@@ -120,6 +120,7 @@ class PreviewStream:
         self.trace = None  # a list -> process() appends (phase, CUDA event) after each phase (bench breakdown)
 
     def _mark(self, name: str) -> None:
+        torch.cuda.nvtx.mark(f"stream.{name}")
         if self.trace is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record()

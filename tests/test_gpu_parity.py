@@ -868,3 +868,19 @@ def test_circle_mask_spans_random(P, cuda):
         v = rng.integers(1, 256, size=shape, dtype=np.uint8)
         got = P.apply_circle_mask(P.Volume(v), C(cx=cx, cy=cy, r=r), margin=m).voxels
         assert np.array_equal(got, O.apply_circle_mask(v, cx, cy, r, m)), (shape, cx, cy, r, m)
+
+
+def test_every_kernel_small_shapes_blocking_launches(P, cuda):
+    """tools/sanitize_smoke.py (every kernel on small and ragged shapes: the fused pass u8/u16
+    incl. the cooperative step, LUT kernels, general downscale paths, circle mask, PNG filter +
+    deflate, atlas encode/decode, every render path, the config-5 processor) with
+    CUDA_LAUNCH_BLOCKING=1 in a fresh process: no launch or execution error.  (compute-sanitizer
+    is closed on this GPU pool; this is the in-tree stand-in.)"""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / "sanitize_smoke.py")], capture_output=True, text=True,
+                       timeout=600, env={**os.environ, "CUDA_LAUNCH_BLOCKING": "1"})
+    assert r.returncode == 0 and "sanitize smoke done" in r.stdout, r.stderr[-2000:]

@@ -25,11 +25,21 @@ v16 = synth.generate(synth.small((64, 64, 128), dtype="u16", seed=2))
 lut16, _ = dev.artifact_lut_fused(v16)
 h16 = torch.zeros(4096, dtype=torch.int64, device="cuda")
 dev.preview(v16, lut16, {1: "xyz", 4: AtlasSpec(8, 32, 4, 1)}, hist=h16)
+# the whole step in one cooperative launch (in-kernel artifact LUT + grid barrier), u8 and u16
+# (the u16 hot window chosen from each CTA's first tile; its LUT staged in the level-1 sum buffers)
+dev.preview_step(v8, {1: AtlasSpec(64, 512, 8, 1), 2: "xyz", 3: AtlasSpec(16, 64, 4, 1)})
+dev.preview_step(v16, {1: "xyz", 2: AtlasSpec(32, 256, 8, 1), 4: AtlasSpec(8, 32, 4, 1)})
 # stand-alone kernels
 dev.hist_u8(v8, (3, 40))
 dev.lut_apply_u8(v8[:, :, :37].contiguous(), lut, hist=hist)
 dev.lut_apply_u16(v16[:, :, :37].contiguous(), lut16, hist=h16)      # any-length u16 filter o rescale
-dev.downscale(v8, (37, 29, 23))
+dev.downscale(v8, (37, 29, 23))               # warp-per-row kernel, x cells <= 4
+dev.downscale(v8, (64, 48, 32))                # x cells <= 2 (1.5:1, config 5's level-1 ratio), 4-output stores
+dev.downscale(v8, (5, 7, 3))                   # wide cells: the float rounding path
+dev.circle_mask(v8, 40.5, 30.25, 25.0 ** 2)
+f = dev.png_filter(dev.encode_atlas(v8[:64, :64, :64].contiguous(), AtlasSpec(64, 512, 8, 1)))
+from paper_2311_15038_b200.png import deflate_device  # noqa: E402
+deflate_device(f)
 dev.encode_atlas(v8[:48, :48, :48].contiguous(), AtlasSpec(64, 512, 8, 1))
 dev.decode_atlas(dev.encode_atlas(v8[:64, :64, :64].contiguous(), AtlasSpec(64, 512, 8, 1)), AtlasSpec(64, 512, 8, 1))
 # renders: exact fp64 modes, fp32 MIP (row planes) and alpha (texture)
