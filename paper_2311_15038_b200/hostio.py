@@ -23,6 +23,7 @@ drop-in call crosses PCIe.  Two things keep that cost at the PCIe floor:
 from __future__ import annotations
 
 import os
+import sys
 import threading
 import warnings
 import weakref
@@ -61,8 +62,20 @@ class DeviceCache:
 
     @staticmethod
     def cacheable(arr: np.ndarray) -> bool:
-        return (isinstance(arr, np.ndarray) and not arr.flags.writeable and arr.flags.c_contiguous
-                and arr.nbytes >= CACHE_MIN_BYTES and arr.dtype in _NP2T)
+        if not (isinstance(arr, np.ndarray) and arr.flags.c_contiguous and arr.nbytes >= CACHE_MIN_BYTES
+                and arr.dtype in _NP2T):
+            return False
+        # frozen all the way down: a read-only VIEW of a writeable array (Volume(big[a:b])
+        # freezes only the view, volume.py:60-62) can still change through its base -- unless
+        # nothing but the view refers to that base any more (Volume(data.reshape(nz, ny, nx)),
+        # volume.py:249: numpy collapses .base to the owner, so any other view or name of
+        # the owner shows up in its reference count)
+        b = arr.base
+        while isinstance(b, np.ndarray):
+            if b.flags.writeable and sys.getrefcount(b) > 3:  # arr.base + `b` + the argument
+                return False
+            b = b.base
+        return not arr.flags.writeable
 
     def get(self, arr: np.ndarray, device) -> torch.Tensor | None:
         if not self.enabled or not self.cacheable(arr):

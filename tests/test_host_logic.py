@@ -197,3 +197,35 @@ def test_install_binds_reference_error_classes_when_imported_later():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
                        env={**os.environ, "NUMBA_CACHE_DIR": "/tmp/ctp_numba_err_test"})
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
+
+
+def test_device_cache_only_tracks_arrays_frozen_all_the_way_down():
+    """The device-copy cache of the host drop-ins (hostio.DeviceCache) must never serve a
+    stale copy: a read-only view of an array the caller can still write through is not
+    cached (Volume freezes only the view it is given, volume.py:60-62), a view whose base
+    nobody else refers to (Volume(data.reshape(...)), volume.py:249) is."""
+    from paper_2311_15038_b200.hostio import DeviceCache
+
+    def loaded():
+        data = np.zeros(4 << 20, np.uint8)
+        v = data.reshape(4, 1 << 10, 1 << 10)
+        v.setflags(write=False)
+        return v
+
+    v = loaded()
+    assert DeviceCache.cacheable(v)
+    base = v.base                      # the caller got hold of the writeable owner
+    assert not DeviceCache.cacheable(v)
+    del base
+    assert DeviceCache.cacheable(v)
+    big = np.zeros((4, 1 << 20), np.uint8)
+    w = big[1:3]
+    w.setflags(write=False)
+    assert not DeviceCache.cacheable(w)  # big[...] = x would change w
+    big.setflags(write=False)
+    assert DeviceCache.cacheable(w)
+    own = np.zeros(4 << 20, np.uint8)
+    assert not DeviceCache.cacheable(own)
+    own.setflags(write=False)
+    assert DeviceCache.cacheable(own)
+    assert not DeviceCache.cacheable(np.zeros(16, np.uint8))  # too small to track
