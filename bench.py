@@ -73,8 +73,34 @@ class ClockSampler:
         self.rows = []  # (host_time, [fields])
         self.proc = None
         self.t0 = self.t1 = None
+        self.nvml_rows = []  # (host_time, sm_mhz, sm_max_mhz, reasons bitmask): NVML, ~1 ms apart
+        self._nvml_stop = threading.Event()
+        self._nvml_thread = None
+
+    def _nvml_loop(self):
+        """The same counters read in-process through NVML about every millisecond, so that a
+        timed region of a few milliseconds (20 steps of 0.26 ms) still holds several samples."""
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            try:
+                h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(self.gpu).uuid))
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            while not self._nvml_stop.is_set():
+                t = time.time()
+                sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.nvml_rows.append((t, sm, mx, rs))
+                time.sleep(0.0005)
+        except Exception:
+            pass
 
     def __enter__(self):
+        self._nvml_thread = threading.Thread(target=self._nvml_loop, daemon=True)
+        self._nvml_thread.start()
         try:
             cmd = ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                    "-lms", "50"]
@@ -105,6 +131,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         time.sleep(0.2)
+        self._nvml_stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -113,6 +140,23 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        nv = [r for r in self.nvml_rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        if nv:
+            try:
+                import pynvml as nv_
+                bits = {"hw_slowdown": nv_.nvmlClocksEventReasonHwSlowdown,
+                        "hw_thermal_slowdown": nv_.nvmlClocksEventReasonHwThermalSlowdown,
+                        "sw_thermal_slowdown": nv_.nvmlClocksEventReasonSwThermalSlowdown,
+                        "sw_power_cap": nv_.nvmlClocksEventReasonSwPowerCap}
+                mask = 0
+                for r in nv:
+                    mask |= r[3]
+                return {"sm_mhz": statistics.median(r[1] for r in nv), "sm_max_mhz": max(r[2] for r in nv),
+                        "reasons": sorted(n for n, b in bits.items() if mask & b), "samples": len(nv),
+                        "source": "nvml, ~1 ms apart, inside the timed region",
+                        "nvidia_smi_samples": len([1 for t, _ in self.rows if self.t0 <= t <= (self.t1 or t) + 0.06])}
+            except Exception:
+                pass
         rows = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t) + 0.06]
         if not rows and self.rows and self.t0 is not None:  # region shorter than one period: nearest sample
             rows = [min(self.rows, key=lambda tr: abs(tr[0] - self.t0))[1]]

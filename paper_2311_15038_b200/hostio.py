@@ -44,6 +44,9 @@ PINNED_OUT_MIN_BYTES = 1 << 20  # smaller outputs are read back into pageable me
 # staging: NBUF pinned buffers of CHUNK bytes = NBUF concurrent memcpy threads; measured on the
 # B200 box (16 host cores, tools/prof_h2d.py, 1 GiB pageable): 8 x 16 MB 35.9 GB/s, 8 x 32 MB
 # 43-45 GB/s (PCIe pinned copy: 55 GB/s), 12 x 32 MB the same, 128 MB chunks 32 GB/s
+# (round 2, tools/r2_h2d_parts.sh: filling each chunk with 2-8 pool tasks so the first DMA starts
+# sooner changes nothing, 24.1-24.6 ms either way -- the host's memcpy rate beside the DMA reads
+# is the bound, not the start-up of the pipeline)
 CHUNK = int(os.environ.get("CTP_STAGE_CHUNK_MB", "32")) << 20
 NBUF = int(os.environ.get("CTP_STAGE_BUFS", str(min(8, os.cpu_count() or 8))))
 

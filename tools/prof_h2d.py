@@ -9,6 +9,7 @@ ts = []
 for _ in range(5):
     t0 = time.perf_counter(); t = hostio.h2d(a, dev); torch.cuda.synchronize(); ts.append(time.perf_counter() - t0)
 print(f"bufs={hostio.NBUF} chunk={hostio.CHUNK>>20}MB h2d 1 GiB: {min(ts)*1e3:.1f} ms {a.nbytes/min(ts)/1e9:.1f} GB/s")
+if os.environ.get("CTP_PROF_REGISTER") != "1": sys.exit(0)
 # cudaHostRegister in place
 cudart = torch.cuda.cudart()
 ts=[]
