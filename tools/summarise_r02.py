@@ -75,6 +75,12 @@ def kernels(tag: str) -> None:
             lines.append(f"# {name}: missing")
             continue
         lines.append(f"# --- {name}")
+        if name == "secondary":
+            lines.append("# launch order (tools/prof_secondary.py; torch's own fill/scan kernels in between): downscale 1024^3->512^3, "
+                         "c5's 768^2x1024->512^3, encode 512, decode 512, PNG filter, deflate (+ compact), circle span + apply, "
+                         "hist u8 (volume), hist u8 (top slab) + lut_build, lut_apply u8, hist u16, hist u16 (top slab) + lut_build, "
+                         "lut_apply u16, render fp64 SURFACE (2 views), image_hist, render fp64 ADDITIVE (2 views), "
+                         "blend_rows + render_rows<MIP> (8 views), blend_rows + render_rows<ALPHA> (8 views)")
         for d in ncu_rows(rep):
             lines.append(kernel_line(d))
         if name == "fused_c2_step":
