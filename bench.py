@@ -46,7 +46,14 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CLOCK_WARMUP_S = 0.5
+# Untimed steps right before a timed region, so that it does not time the clocks' ramp out of idle.
+# SHORT on purpose: this kernel draws the board's power limit -- after ~0.2 s of back-to-back steps
+# sw_power_cap lowers the SM clock from 1965 to 1800-1900 MHz and the (issue/shared-pipe-bound) pass
+# slows by the same factor (tools/r2_nvml_ab.sh, profiles/r02_clock_warmup_sweep.txt: warm-up 0.02-0.1 s
+# -> 1965 MHz, 74-75% of HBM peak; 0.5 s -> 1785-1920 MHz, 69%).  The headline is therefore the burst
+# figure at max clocks (like MEASURED_PEAKS' best-of-10 copy), and the line carries the sustained one
+# (2000 back-to-back steps, clocks and reasons sampled) beside it as "sustained".
+CLOCK_WARMUP_S = float(os.environ.get("CTP_CLOCK_WARMUP_S", "0.05"))
 METRIC = "pipeline GVoxel/s (hist+filter+slicemaps) & MIP frames/s, % of HBM roofline"
 SCHEMES = (512, 256, 128)
 
@@ -68,8 +75,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, smi: bool = True):
         self.gpu = gpu_index
+        self.smi = smi  # False: NVML thread only (side measurements; no process to spawn)
         self.rows = []  # (host_time, [fields])
         self.proc = None
         self.t0 = self.t1 = None
@@ -99,8 +107,11 @@ class ClockSampler:
             pass
 
     def __enter__(self):
-        self._nvml_thread = threading.Thread(target=self._nvml_loop, daemon=True)
-        self._nvml_thread.start()
+        if os.environ.get("CTP_BENCH_NVML", "1") != "0":
+            self._nvml_thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._nvml_thread.start()
+        if not self.smi:
+            return self
         try:
             cmd = ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                    "-lms", "50"]
@@ -130,7 +141,8 @@ class ClockSampler:
             self.t1 = time.time()
 
     def __exit__(self, *a):
-        time.sleep(0.2)
+        if self.smi:
+            time.sleep(0.2)
         self._nvml_stop.set()
         if self.proc:
             self.proc.terminate()
@@ -139,7 +151,9 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, window=None):
+        if window is not None:
+            self.t0, self.t1 = window
         nv = [r for r in self.nvml_rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
         if nv:
             try:
@@ -188,6 +202,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mip", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--mip-batches", type=int, default=4)
     ap.add_argument("--no-configs", action="store_true", help="skip the c1 / c3 / c4-alpha side measurements")
     args = ap.parse_args()
@@ -242,13 +257,18 @@ def main():
             sh.fused_events = (k0[i], k1[i])
         return sh.step(slab)
 
+    # the clock sampler starts BEFORE the warm-up (spawning nvidia-smi takes ~0.3 s: started
+    # between the warm-up and the timed region, that idle gap let the clocks fall again and the
+    # first timed steps ran ~2% slow -- 20-step runs read 0.726 where 2000-step runs read 0.739)
+    sampler = ClockSampler(local)
+    sampler.__enter__()
     for _ in range(args.warmup):
         step()
     # plus untimed steps for CLOCK_WARMUP_S so the SM clocks have left their idle state (a 20-step
     # timed region is ~5 ms).  N > 1: a fixed count (the steps' collectives pair the ranks' steps)
     n_clock = 0
     t_w = time.perf_counter()
-    while (n_clock < 2000) if world > 1 else (n_clock % 64 or time.perf_counter() - t_w < CLOCK_WARMUP_S):
+    while (n_clock < 256) if world > 1 else (n_clock % 64 or time.perf_counter() - t_w < CLOCK_WARMUP_S):
         step()
         n_clock += 1
         if n_clock % 64 == 0:
@@ -258,11 +278,7 @@ def main():
     if world > 1:
         dist.barrier()
     _lib.launch_count(reset=True)
-    sampler = ClockSampler(local)
-    with sampler:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+    try:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         sampler.mark(True)
@@ -274,9 +290,30 @@ def main():
         sampler.mark(False)
         if world > 1:
             dist.barrier()
-    launches = _lib.launch_count()
-    ms = t0.elapsed_time(t1)
-    kern_ms = [a.elapsed_time(b) for a, b in zip(k0, k1)]
+        launches = _lib.launch_count()
+        ms = t0.elapsed_time(t1)
+        kern_ms = [a.elapsed_time(b) for a, b in zip(k0, k1)]
+        clocks = sampler.summary()
+        # the sustained figure: 2000 more back-to-back steps (~0.5 s: the power limiter has settled)
+        sustained = None
+        if world == 1 and not args.no_sustained:
+            n_s = 2000
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            sh.fused_events = None
+            w0 = time.time()
+            s0.record(stream)
+            for _ in range(n_s):
+                step()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            w1 = time.time()
+            s_ms = s0.elapsed_time(s1) / n_s
+            sustained = {"steps": n_s, "ms_per_step": s_ms, "value": nx * ny * nz / (s_ms * 1e-3) / 1e9,
+                         "unit": "GVoxel/s", "clocks": sampler.summary((w0, w1)),
+                         "note": "the same step back to back for ~0.5 s right after the timed region (whole steps, "
+                                 "host launch gaps included)"}
+    finally:
+        sampler.__exit__(None, None, None)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -359,7 +396,8 @@ def main():
             "e2e_session": e2e_session,
             "gpu_launches": launches,
             "clock_warmup_steps": n_clock,
-            "clocks": sampler.summary(),
+            "clocks": clocks,
+            "sustained": sustained,
             "mip": mip,
             "replicas": replicas,
             "c3_zslab": c3_zslab,
@@ -663,22 +701,30 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
         sr = ShardedRender(spec.shape, dim, DeviceRenderCompute(), 0, 1, device)
     local = synth.generate(spec, z_range=(sr.h0, sr.h1), device=device)
     sr.render(local, views, channels=4, fp32=True)   # warmup (row planes allocated once)
-    if world == 1:
-        _warm_clocks(lambda: sr.render(local, views, channels=4, fp32=True))
-    else:  # every rank renders the same number of warm-up batches (the batches synchronise the ranks)
-        for _ in range(8):
-            sr.render(local, views, channels=4, fp32=True)
+    # 8 untimed batches (~0.3 s; N > 1: the batches synchronise the ranks, so a fixed count).  Not only
+    # for the clocks: for a few batches after the process freed and allocated gigabytes (the legs
+    # before this one; the 2 GiB row planes), single batches take 45-135 ms instead of 39 with the
+    # clocks at maximum and no throttle reason (tools/r2_mip_bimodal.py, profiles/r02_mip_hiccups.txt)
+    # -- 4 timed batches right behind 2 warm-up batches caught one in about one run in three
+    # (924 vs 544-574 frames/s); "batch_ms" lists every timed batch
+    for _ in range(8):
+        sr.render(local, views, channels=4, fp32=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.mip_batches):
-        sr.render(local, views, channels=4, fp32=True)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.mip_batches + 1)]
+    with ClockSampler(device.index or 0, smi=False) as cs:
+        time.sleep(0.01)  # the NVML thread is up
+        cs.mark(True)
+        ev[0].record()
+        for q in range(args.mip_batches):
+            sr.render(local, views, channels=4, fp32=True)
+            ev[q + 1].record()
+        torch.cuda.synchronize()
+        cs.mark(False)
+    mip_clocks = cs.summary()
+    ms = ev[0].elapsed_time(ev[-1])
+    batch_ms = [ev[q].elapsed_time(ev[q + 1]) for q in range(args.mip_batches)]
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -696,14 +742,15 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
     return {"value": frames / (ms * 1e-3), "unit": "frames/s", "ms_per_frame": ms / frames,
             "gsamples_per_s": frames * dim * dim * steps / (ms * 1e-3) / 1e9, "steps_per_ray": steps,
             "image": "1024^2 RGBA8", "volume": "1024^3 u8 (config-4 generator)", "views_per_batch": 36,
-            "batches": args.mip_batches, "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
+            "batches": args.mip_batches, "batch_ms": batch_ms, "clocks": mip_clocks,
+            "precision": "fp32 (8.8 fixed-point row planes), tolerance 1/255",
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
             "bound": "texture pipe: one tld4 gather per sample (ncu: profiles/r01_render_c4_mip_ncu.txt)",
             "scaling": "weak" if mode == "replicas" else "strong", "mode": mode,
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + how}
 
 
-def _warm_clocks(fn, seconds: float = 0.5):
+def _warm_clocks(fn, seconds: float = CLOCK_WARMUP_S):
     """Run ``fn`` back to back for ``seconds``: SM clocks drop while the GPU idles (e.g. during
     a host-side leg), and a side measurement of a few ms would otherwise time the ramp."""
     import torch

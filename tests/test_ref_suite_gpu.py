@@ -1,0 +1,49 @@
+"""The REFERENCE's own test suite on the GPU, with its hot path rebound by ``install()``
+("a drop-in for that path"): ctprev's tests for volume / mask / slicemap /
+render / pipeline plus its ten acceptance criteria (tests/test_volume.py, test_mask.py,
+test_slicemap.py, test_render.py, test_pipeline.py, test_acceptance.py under
+/root/reference/pkg) run UNMODIFIED in a subprocess whose pytest loads
+tools/ref_suite_plugin.py: ``install()`` is called before any test module is imported, so
+every ``from ctprev.volume import ...`` binds the B200 drop-ins, and the session ends with
+the number of kernels launched through libctprev_b200.so.
+
+The reference's tests are not part of this repository: they are read from the mounted
+reference (this container) or from ``baseline/_ref_tests`` -- a git-ignored copy that
+``tools/r2_ref_suite.sh`` places next to the installed reference (``baseline/_ref``) so that
+it travels to the GPU box; the test is skipped where neither exists."""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+FILES = ["test_volume.py", "test_mask.py", "test_slicemap.py", "test_render.py", "test_pipeline.py",
+         "test_acceptance.py"]
+
+
+@pytest.mark.gpu
+def test_reference_test_suite_passes_with_the_b200_path_installed(cuda, tmp_path):
+    ref = ROOT / "baseline" / "_ref"
+    tests = next((d for d in (ROOT / "baseline" / "_ref_tests", Path("/root/reference/pkg/tests"))
+                  if (d / "test_volume.py").is_file()), None)
+    if tests is None or not (ref / "ctprev").is_dir():
+        pytest.skip("the reference's tests (baseline/_ref_tests) or its install (baseline/_ref) are not present")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(ROOT / "tools"), str(ROOT), str(ref)])
+    env.setdefault("NUMBA_CACHE_DIR", "/tmp/ctp_ref_numba_cache")
+    r = subprocess.run([sys.executable, "-m", "pytest", *FILES, "-q", "-p", "ref_suite_plugin", "-p", "no:cacheprovider",
+                        "--basetemp", str(tmp_path / "ref")], cwd=tests, env=env, capture_output=True, text=True,
+                       timeout=1800)
+    tail = r.stdout[-3000:]
+    assert r.returncode == 0, tail + r.stderr[-2000:]
+    m = re.search(r"(\d+) passed", r.stdout)
+    assert m and int(m.group(1)) >= 130 and "failed" not in r.stdout, tail
+    for k in range(1, 11):  # the ten acceptance criteria of the reference (tests/conftest.py summary)
+        assert re.search(rf"criterion\s+{k}: PASS", r.stdout), tail
+    lm = re.search(r"(\d+) binding sites rebound, (\d+) kernel launches", r.stdout)
+    assert lm and int(lm.group(1)) > 0 and int(lm.group(2)) > 100, tail  # the device path ran

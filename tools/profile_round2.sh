@@ -9,9 +9,9 @@ mkdir -p $OUT
 python bench.py --steps 20 --warmup 5 > $OUT/bench.jsonl 2> $OUT/bench.err; echo "bench rc=$?"
 python bench.py --impl reference --steps 20 --warmup 5 > $OUT/bench_reference.jsonl 2> $OUT/bench_reference.err; echo "reference rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
-  python bench.py --steps 20 --warmup 3 --no-mip --no-cpu-baseline --no-configs --no-e2e > $OUT/launches.log 2>&1; echo "launch list rc=$?"
+  python bench.py --steps 20 --warmup 3 --no-mip --no-cpu-baseline --no-configs --no-e2e --no-sustained > $OUT/launches.log 2>&1; echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:preview_kernel -s 5 -c 1 -o $OUT/fused_c2_step -f \
-  python bench.py --steps 3 --warmup 3 --no-mip --no-e2e --no-cpu-baseline --no-configs > $OUT/ncu_c2.log 2>&1; echo "ncu c2 rc=$?"
+  python bench.py --steps 3 --warmup 3 --no-mip --no-e2e --no-cpu-baseline --no-configs --no-sustained > $OUT/ncu_c2.log 2>&1; echo "ncu c2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:preview_kernel -s 1 -c 1 -o $OUT/fused_c3_u16 -f \
   python tools/prof_preview.py --config c3 --schemes 1024,512,256,128 --reps 2 > $OUT/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:^(?!synth)' -c 40 -o $OUT/secondary -f \
