@@ -390,6 +390,7 @@ def main():
                                     "(artifact-LUT phase + fused hist/filter/pyramid/atlas pass)") if world == 1 else
                                    ("preview_kernel<uint8_t,3,1024 thr> on this rank's z-slab (fused hist/filter/"
                                     "pyramid/atlas pass, atlas rows stored into rank 0's atlases)"), "kernel_ms": kmean,
+                         "kernel_ms_min_median_max": [min(kern_ms), statistics.median(kern_ms), max(kern_ms)],
                          "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -730,6 +731,26 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     frames = 36 * args.mip_batches * (world if mode == "replicas" else 1)
+    # the same number of frames with NO opposite azimuths in the batch (36 views 5 degrees apart over
+    # [0, 180)): every view walks its own rays -- the turntable above renders each opposite pair once
+    independent = None
+    if world == 1:
+        half = [ViewParams(azimuth_deg=5.0 * k, image_dim=dim, steps=steps, mode="mip") for k in range(36)]
+        for _ in range(2):
+            sr.render(local, half, channels=4, fp32=True)
+        torch.cuda.synchronize()
+        hv = [torch.cuda.Event(enable_timing=True) for _ in range(args.mip_batches + 1)]
+        hv[0].record()
+        for q in range(args.mip_batches):
+            sr.render(local, half, channels=4, fp32=True)
+            hv[q + 1].record()
+        torch.cuda.synchronize()
+        h_ms = hv[0].elapsed_time(hv[-1])
+        independent = {"value": 36 * args.mip_batches / (h_ms * 1e-3), "unit": "frames/s",
+                       "ms_per_frame": h_ms / (36 * args.mip_batches),
+                       "batch_ms": [hv[q].elapsed_time(hv[q + 1]) for q in range(args.mip_batches)],
+                       "views": "36 azimuths 5 degrees apart over [0, 180): no opposite pairs, every view rendered on "
+                                "its own (one tld4 gather per sample, texture-pipe bound)"}
     del local
     sr.close()
     from paper_2311_15038_b200 import device as dev
@@ -747,6 +768,10 @@ def bench_mip(args, device, rank, world, dist, mode: str = "single"):
             "hbm_frac_volume_bytes": (spec.nbytes * frames / (ms * 1e-3) / 1e9) / _peaks()[0]["hbm_gbs"],
             "bound": "texture pipe: one tld4 gather per sample (ncu: profiles/r01_render_c4_mip_ncu.txt)",
             "scaling": "weak" if mode == "replicas" else "strong", "mode": mode,
+            "turntable": "36 azimuths 10 degrees apart over 360: the 18 opposite pairs (a, a + 180) are mirror images "
+                         "of each other (orthographic MIP, elevation 0) and are rendered once, stored twice "
+                         "(csrc/render.cu pair_opposite_views; every view within 1/255 of its own oracle render)",
+            "independent_views": independent,
             "includes": "per-batch row-plane build (2 B/voxel/row) + 36 frames" + how}
 
 

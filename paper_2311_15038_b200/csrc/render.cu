@@ -43,6 +43,11 @@ struct ViewBatch {  // passed by value (kernel parameter space), <= 64 views per
   ViewDev v[kMaxViews];
   int64_t vstride;  // bytes between consecutive views' first rows in `out`
   int32_t peer;     // `out` is a peer GPU's memory: system-scope fence after the stores
+  // fp32 MIP on the row planes: grid.z walks the PRIMARY views prim[0..]; mirror[z] >= 0 names the
+  // view at azimuth + 180 degrees, whose image is the primary's mirrored left-right (see
+  // pair_opposite_views) and is stored by the same thread.  Identity / -1 everywhere else.
+  int8_t prim[kMaxViews];
+  int8_t mirror[kMaxViews];
 };
 
 // 2x2 footprint of one slice of a layered u8 texture (clamp addressing): the
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
                                                          int row1, uint8_t* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
-  const int view = blockIdx.z;
+  const int view = views.prim[blockIdx.z];
   if (i >= dim || j >= row1) return;
   const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
@@ -371,6 +376,12 @@ __global__ void __launch_bounds__(128) render_tex_kernel(cudaTextureObject_t tex
     const uint8_t o = (uint8_t)(int)floorf(fminf(m, 255.f) + 0.5f);
     if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(o, o, o, 255);
     else dst[0] = o;
+    const int mv = views.mirror[blockIdx.z];
+    if (mv >= 0) {  // the opposite azimuth sees this ray's sample set from the other end: pixel dim-1-i
+      uint8_t* d2 = out + (int64_t)mv * views.vstride + ((int64_t)(j - row0) * dim + (dim - 1 - i)) * ch;
+      if (ch == 4) *reinterpret_cast<uchar4*>(d2) = make_uchar4(o, o, o, 255);
+      else d2[0] = o;
+    }
   } else {
     if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(to_u8_unit<float>(C0), to_u8_unit<float>(C1),
                                                               to_u8_unit<float>(C2), to_u8_unit<float>(A));
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t te
                                                           const uint16_t* __restrict__ bmax, int nbx, int nby, int skip) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = row0 + blockIdx.y;
-  const int view = blockIdx.z;
+  const int view = views.prim[blockIdx.z];
   if (i >= dim || j >= row1) return;
   const ViewDev& V = views.v[view];
   const RenderGeom& G = V.g;
@@ -588,6 +599,12 @@ __global__ void __launch_bounds__(128) render_rows_kernel(cudaTextureObject_t te
     const uint8_t o = (uint8_t)(int)floorf(fminf(m, 255.f) + 0.5f);
     if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(o, o, o, 255);
     else dst[0] = o;
+    const int mv = views.mirror[blockIdx.z];
+    if (mv >= 0) {  // the opposite azimuth sees this ray's sample set from the other end: pixel dim-1-i
+      uint8_t* d2 = out + (int64_t)mv * views.vstride + ((int64_t)(j - row0) * dim + (dim - 1 - i)) * ch;
+      if (ch == 4) *reinterpret_cast<uchar4*>(d2) = make_uchar4(o, o, o, 255);
+      else d2[0] = o;
+    }
   } else {
     if (ch == 4) *reinterpret_cast<uchar4*>(dst) = make_uchar4(to_u8_unit<float>(C0), to_u8_unit<float>(C1),
                                                               to_u8_unit<float>(C2), to_u8_unit<float>(A));
@@ -698,6 +715,36 @@ __global__ void image_hist_kernel(const uint8_t* __restrict__ imgs, int64_t pixe
     if (hs[b]) atomicAdd(hist + (int64_t)img * 256 + b, (unsigned long long)hs[b]);
 }
 
+// Opposite azimuths of an orthographic MIP are mirror images: for theta' = theta + 180 degrees the
+// march direction and the image's right vector both change sign (render.py:212-216), so pixel
+// i' = dim-1-i of row j starts on the SAME line (o' = r' wx' = r wx = o) and, because steps * dt =
+// 2R exactly (render.py:222), its sample k' = steps-1-k sits at t' = -R + (k'+1/2) dt = -t_k on the
+// reversed direction: the same point.  Both rays take the maximum over the same sample set, so a
+// turntable renders each opposite pair once and stores it twice.  (Only for the order-independent
+// maximum on the fp32 path, whose contract is max-abs 1/255 -- positions agree to fp rounding;
+// the fp64 paths keep the reference's per-view operation order bit for bit.)  n_prim primaries
+// come out in vb.prim, each with its mirror or -1.
+static int pair_opposite_views(const ViewDev* hv, int n_views, ViewBatch& vb, bool enable) {
+  bool used[kMaxViews] = {false};
+  int n_prim = 0;
+  for (int q = 0; q < n_views; q++) {
+    if (used[q]) continue;
+    used[q] = true;
+    int m = -1;
+    for (int p = q + 1; enable && p < n_views && m < 0; p++) {
+      if (used[p] || hv[p].steps != hv[q].steps || hv[p].channels != hv[q].channels) continue;
+      const RenderGeom &A = hv[q].g, &B = hv[p].g;
+      const double e = 1e-12;
+      if (fabs(A.dx + B.dx) < e && fabs(A.dy + B.dy) < e && fabs(A.rx + B.rx) < e && fabs(A.ry + B.ry) < e) m = p;
+    }
+    if (m >= 0) used[m] = true;
+    vb.prim[n_prim] = (int8_t)q;
+    vb.mirror[n_prim] = (int8_t)m;
+    n_prim++;
+  }
+  return n_prim;
+}
+
 // Slices a row band reads, for any mode and either precision: the trilinear
 // pair around uz(j) (render.py:105-111) plus the surface gradient's +-1 and a
 // one-slice margin for the fp32 floor (render.py:185-192).
@@ -788,21 +835,35 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
               (long long)vstride, (long long)band);
   vb.vstride = vstride ? vstride : band;
   vb.peer = (out_flags & CTP_OUT_PEER) ? 1 : 0;
+  for (int q = 0; q < kMaxViews; q++) {
+    vb.prim[q] = (int8_t)q;
+    vb.mirror[q] = -1;
+  }
   dim3 grid((dim + 127) / 128, (unsigned)(row1 - row0), (unsigned)n_views);
   const bool tex_path = v0.fp32 && (v0.mode == CTP_MODE_MIP || v0.mode == CTP_MODE_ALPHA) && snz <= 2048 &&
                         nx <= 32768 && ny <= 32768;
   if (tex_path) {
     // row planes when they fit comfortably (4 B per voxel per image row)
     std::unique_lock<std::mutex> lock(g_planes_mu);  // held until the planes' last reader finished
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
     int dev_id = 0;
     cudaGetDevice(&dev_id);
-    if (dev_id >= 0 && dev_id < kMaxDevices && g_planes[dev_id])  // cached planes count as free
-      free_b += (size_t)g_planes[dev_id]->rows * g_planes[dev_id]->ny * g_planes[dev_id]->nx * 2;
+    const bool in_range = dev_id >= 0 && dev_id < kMaxDevices;
     const size_t plane_bytes = (size_t)(row1 - row0) * (size_t)nx * (size_t)ny * 2;
+    // planes of this shape are already allocated: no free-memory query (cudaMemGetInfo is a
+    // driver round trip that was seen to block for tens of milliseconds while the driver was
+    // still working through gigabytes freed earlier by the process -- the occasional 45-135 ms
+    // batch of profiles/r02_mip_hiccups.txt)
+    bool fits = in_range && g_planes[dev_id] && g_planes[dev_id]->rows == row1 - row0 && g_planes[dev_id]->ny == ny &&
+                g_planes[dev_id]->nx == nx;
+    if (!fits) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      if (in_range && g_planes[dev_id])  // cached planes count as free
+        free_b += (size_t)g_planes[dev_id]->rows * g_planes[dev_id]->ny * g_planes[dev_id]->nx * 2;
+      fits = plane_bytes < free_b / 2;
+    }
     const char* rp_env = getenv("CTP_RENDER_ROWPLANES");  // "0" forces the two-gather path
-    if (!(rp_env && rp_env[0] == '0') && row1 - row0 <= 2048 && plane_bytes < free_b / 2) {
+    if (!(rp_env && rp_env[0] == '0') && row1 - row0 <= 2048 && fits) {
       RowPlanes* rpp = nullptr;
       int rc = get_planes(&rpp, row1 - row0, ny, nx);
       if (rc != CTP_OK) return rc;
@@ -815,10 +876,13 @@ static int render_impl(const uint8_t* vol, int64_t zb, int64_t snz, int64_t nz, 
       blend_rows_kernel<<<bg, kBlendThreads, 0, st>>>(vol, (int)zb, (int)nx, (int)ny, (int)nz, G0.big_r, G0.px_size, G0.inv_vx,
                                                    (int)row0, rp.surf, rp.bmax, nbx, nby);
       CTP_CUDA_CHECK_LAUNCH("blend_rows_kernel");
-      if (v0.mode == CTP_MODE_MIP)
-        render_rows_kernel<CTP_MODE_MIP><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
-                                                               (int)row1, out, rp.bmax, nbx, nby, skip);
-      else
+      if (v0.mode == CTP_MODE_MIP) {
+        const char* mi_env = getenv("CTP_RENDER_MIRROR");  // "0": every view on its own
+        dim3 pgrid = grid;
+        pgrid.z = (unsigned)pair_opposite_views(hv, n_views, vb, !(mi_env && mi_env[0] == '0'));
+        render_rows_kernel<CTP_MODE_MIP><<<pgrid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
+                                                                (int)row1, out, rp.bmax, nbx, nby, skip);
+      } else
         render_rows_kernel<CTP_MODE_ALPHA><<<grid, 128, 0, st>>>(rp.tex, (int)nx, (int)ny, (int)nz, vb, dim, (int)row0,
                                                                  (int)row1, out, rp.bmax, nbx, nby, skip);
       CTP_CUDA_CHECK_LAUNCH("render_rows_kernel");

@@ -368,6 +368,43 @@ def test_mip_fp64_exact_and_fp32_within_one(P, golden):
         assert int(np.abs(g32.astype(int) - ref).max()) <= 1
 
 
+def test_mip_turntable_opposite_views_rendered_once(P):
+    """fp32 MIP turntable: a view and the one at azimuth + 180 degrees are rendered ONCE and stored
+    mirrored (csrc/render.cu pair_opposite_views).  Every view -- paired or not, RGBA or gray --
+    stays within 1/255 of the oracle's independent render of that view, paired and unpaired
+    (CTP_RENDER_MIRROR=0) batches agree within 1, and the exact fp64 path is untouched."""
+    import os
+    rng = np.random.default_rng(23)
+    vol = np.clip(np.rint(rng.normal(40, 25, (44, 52, 60))), 0, 255).astype(np.uint8)
+    vol[10:30, 20:40, 15:45] = np.clip(vol[10:30, 20:40, 15:45].astype(int) + 120, 0, 255).astype(np.uint8)
+    azs = [0.0, 30.0, 45.0, 180.0, 210.0, 300.0, 120.0, 7.5, 187.5]  # pairs (0,180) (30,210) (300,120) (7.5,187.5); 45 alone
+    dim, steps = 56, 150
+    ps = [P.ViewParams(azimuth_deg=a, image_dim=dim, steps=steps, mode="mip") for a in azs]
+    refs = [O.render_mip(vol, a, dim, steps) for a in azs]
+    V = P.Volume(vol)
+    for ch in (1, 4):
+        paired = P.render_views(V, ps, channels=ch, fp32=True)
+        os.environ["CTP_RENDER_MIRROR"] = "0"
+        try:
+            single = P.render_views(V, ps, channels=ch, fp32=True)
+        finally:
+            del os.environ["CTP_RENDER_MIRROR"]
+        for k, ref in enumerate(refs):
+            a = paired[k] if ch == 1 else paired[k][..., 0]
+            b = single[k] if ch == 1 else single[k][..., 0]
+            assert int(np.abs(a.astype(int) - ref.astype(int)).max()) <= 1, (ch, azs[k])
+            assert int(np.abs(b.astype(int) - ref.astype(int)).max()) <= 1, (ch, azs[k])
+            assert int(np.abs(a.astype(int) - b.astype(int)).max()) <= 1, (ch, azs[k])
+            if ch == 4:
+                assert np.array_equal(paired[k][..., 1], a) and np.array_equal(paired[k][..., 2], a)
+                assert (paired[k][..., 3] == 255).all()
+    # a view's opposite really is its mirror image (what the pairing relies on), in the oracle itself
+    assert int(np.abs(refs[0].astype(int) - refs[3][:, ::-1].astype(int)).max()) <= 1
+    exact = P.render_views(V, ps, channels=1, fp32=False)
+    for k, ref in enumerate(refs):
+        assert np.array_equal(exact[k], ref)
+
+
 def test_alpha_fp64_and_fp32_within_one(P):
     rng = np.random.default_rng(11)
     vol = np.clip(np.rint(rng.normal(60, 40, (40, 48, 56))), 0, 255).astype(np.uint8)
