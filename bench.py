@@ -277,10 +277,16 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    _lib.launch_count(reset=True)
     try:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        # one more untimed step behind the barrier: the device is idle after the synchronize, so the
+        # first timed step would carry the host's launch path (~50 us: attribute + occupancy queries,
+        # tensor-map encode, cooperative launch) inside its event pair and inside a 5 ms region
+        # (per-step kernel times read 0.247 / 0.248 / 0.307 ms min / median / max); with this step
+        # in flight the host is one step ahead, as it is for every later step
+        step()
+        _lib.launch_count(reset=True)
         sampler.mark(True)
         t0.record(stream)
         for i in range(args.steps):
