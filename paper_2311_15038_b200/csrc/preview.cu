@@ -34,6 +34,7 @@
 #include <stdlib.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <atomic>
 #include <mutex>
 #include <cooperative_groups.h>
 #include "ctp_common.cuh"
@@ -790,13 +791,22 @@ static int launch_k(const PvArgs& a, const CUtensorMap& map, int grid, cudaStrea
     return CTP_E_UNSUPPORTED;
   } else {
   auto kern = preview_kernel<T, L, THREADS, NST, MAXU, WANT0, POW2>;
-  CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  // once per kernel variant and device (function attributes are per context): the dynamic
+  // shared-memory limit and the resident CTAs per SM -- two driver round trips off every
+  // later launch's host path (config 1's step is 16 us on the device)
+  static std::atomic<int> per_sm_of[64];
+  int dev = 0;
+  CTP_CUDA_CALL(cudaGetDevice(&dev));
+  int per_sm = (dev >= 0 && dev < 64) ? per_sm_of[dev].load(std::memory_order_acquire) : 0;
+  if (per_sm == 0) {
+    CTP_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CTP_CUDA_CALL(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, sm));
+    CTP_REQUIRE(per_sm >= 1, CTP_E_CUDA, "preview: kernel does not fit on an SM");
+    if (dev >= 0 && dev < 64) per_sm_of[dev].store(per_sm, std::memory_order_release);
+  }
   if (a.top != nullptr) {
     // the in-kernel LUT step has one grid barrier: a cooperative launch
     // guarantees every CTA is resident (one per SM here)
-    int per_sm = 0;
-    CTP_CUDA_CALL(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, sm));
-    CTP_REQUIRE(per_sm >= 1, CTP_E_CUDA, "preview: kernel does not fit on an SM");
     if (grid > per_sm * num_sms()) grid = per_sm * num_sms();
     CUtensorMap map_copy = map;
     PvArgs a_copy = a;
