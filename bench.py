@@ -84,6 +84,7 @@ class ClockSampler:
         self.nvml_rows = []  # (host_time, sm_mhz, sm_max_mhz, reasons bitmask): NVML, ~1 ms apart
         self._nvml_stop = threading.Event()
         self._nvml_thread = None
+        self._closed = False
 
     def _nvml_loop(self):
         """The same counters read in-process through NVML about every millisecond, so that a
@@ -141,6 +142,9 @@ class ClockSampler:
             self.t1 = time.time()
 
     def __exit__(self, *a):
+        if self._closed:  # idempotent: main() also registers it with atexit
+            return
+        self._closed = True
         if self.smi:
             time.sleep(0.2)
         self._nvml_stop.set()
@@ -262,6 +266,8 @@ def main():
     # first timed steps ran ~2% slow -- 20-step runs read 0.726 where 2000-step runs read 0.739)
     sampler = ClockSampler(local)
     sampler.__enter__()
+    import atexit
+    atexit.register(sampler.__exit__, None, None, None)  # the nvidia-smi child never outlives a failed run
     for _ in range(args.warmup):
         step()
     # plus untimed steps for CLOCK_WARMUP_S so the SM clocks have left their idle state (a 20-step
