@@ -20,7 +20,7 @@ filtered volume) + their slicemap atlases (8x4096^2, 4x2048^2, 2x1024^2).
   mip    = config-4 MIP frames/s (36 azimuths, 1024^2 RGBA8, 0.5-voxel steps,
            1024^3); N > 1: image rows split with the volume replicated (+ sort-last
            z-slab bands and replicas as side keys).
-N > 1 side keys: "replicas" (one c2 volume per rank, weak) and "c3_zslab"
+N > 1 side keys: "replicas" (one c2 volume per rank, weak), "c5_replicas" (config 5: one volume per GPU) and "c3_zslab"
 (config 3, one 16 GiB u16 volume z-slab sharded).  N = 1 side keys under
 "other_configs": c1, c3, c4 alpha / additive, c5, ingest, PNG.
 
@@ -350,7 +350,7 @@ def main():
 
     # ---- N > 1 side measurements: every rank reduces its OWN c2 volume (replicas: weak, no
     # data-path collective), and config 3 (one 16 GiB u16 volume) z-slab sharded
-    replicas = c3_zslab = None
+    replicas = c3_zslab = c5_replicas = None
     if world > 1:
         sh.close()
         del slab, sh
@@ -358,6 +358,7 @@ def main():
         replicas = bench_replicas(args, spec, schemes, level_of, plan, device, rank, world, dist)
         if not args.no_configs:
             c3_zslab = bench_c3_zslab(device, rank, world, dist)
+            c5_replicas = bench_c5_replicas(device, rank, world, dist)
 
     # ---- e2e: the reference-facing drop-in calls on a pageable host Volume (N > 1: one volume
     # per rank), and the host-buffer session on a pinned volume (side key)
@@ -414,6 +415,7 @@ def main():
             "mip": mip,
             "replicas": replicas,
             "c3_zslab": c3_zslab,
+            "c5_replicas": c5_replicas,
             "other_configs": others,
         }
         print(json.dumps(line))
@@ -639,6 +641,97 @@ def bench_c3_zslab(device, rank, world, dist, steps: int = 5):
             "gvoxel_per_s": nx * ny * nz / ms / 1e6,
             "collectives": "LUT all-reduce from the top-slab owner, histogram all-reduce (NCCL), atlas rows stored "
                            "into rank 0's atlases by the fused kernels (CUDA IPC peer mapping)"}
+
+
+def bench_c5_replicas(device, rank, world, dist, n_vol: int = 8):
+    """N > 1 side key: BASELINE config 5 as it is worded -- a stream of 1536^2 x 2048 12-bit volumes,
+    ONE VOLUME PER GPU, data-parallel (independent objects: no data-path collective), aggregate
+    volumes/min and GVoxel/s = all ranks' volumes / the slowest rank's time.  Resident (each rank's
+    volume in HBM), and end to end from pinned host memory (H2D of volume i+1 on a copy stream while
+    volume i is reduced; every product read back)."""
+    import torch
+    from paper_2311_15038_b200 import synth
+    from paper_2311_15038_b200.stream import PreviewStream
+    spec = synth.config("c5", seed=rank)
+    vol = synth.generate(spec, device=device)
+    ps = PreviewStream(spec.shape, torch.uint16, device=device)
+    for _ in range(3):
+        ps.process(vol)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(n_vol):
+        ps.process(vol)
+    a1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / n_vol  # per volume per rank (slowest rank)
+    out = {"workload": f"c5: 1536^2 x 2048 12-bit u16 volumes, one per GPU x{world} (hist + filter o rescale + L1..L4 + "
+                       "SURVEY s8(d) atlases + 36-view 512^2 MIP strip per volume), no data-path collective",
+           "scaling": "weak", "ms_per_volume_per_gpu": ms, "volumes_per_min": world * 60000.0 / ms,
+           "gvoxel_per_s": world * vol.numel() / ms / 1e6}
+    # end to end from pinned host memory (9 GiB pinned per rank): only if EVERY rank got its buffers
+    # (the timed loop holds collectives)
+    host = host_out = bufs = None
+    try:
+        host = torch.empty(spec.shape, dtype=torch.uint16, pin_memory=True)
+        host.copy_(vol)
+        bufs = [vol, torch.empty_like(vol)]
+        host_out = torch.empty(ps.product_bytes, dtype=torch.uint8, pin_memory=True)
+        ok = 1
+    except Exception as e:
+        ok, err = 0, repr(e)[:200]
+    okt = torch.tensor([ok], dtype=torch.int32, device=device)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if int(okt.item()) == 0:
+        out["e2e"] = {"error": err if not ok else "another rank could not allocate its pinned buffers"}
+    else:
+        cs = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        done = [torch.cuda.Event() for _ in range(2)]
+        loaded = [torch.cuda.Event() for _ in range(2)]
+        n_e = 4
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        with torch.cuda.stream(cs):
+            cs.wait_event(e0)
+            bufs[0].copy_(host, non_blocking=True)
+            loaded[0].record(cs)
+        for q in range(n_e):
+            b = q % 2
+            if q + 1 < n_e:
+                with torch.cuda.stream(cs):
+                    if q >= 1:
+                        cs.wait_event(done[1 - b])
+                    bufs[1 - b].copy_(host, non_blocking=True)
+                    loaded[1 - b].record(cs)
+            main.wait_event(loaded[b])
+            r = ps.process(bufs[b])
+            done[b].record(main)
+            o = 0
+            for tt in list(r.atlases.values()) + [r.thumbs]:
+                host_out[o:o + tt.numel()].copy_(tt.reshape(-1), non_blocking=True)
+                o += tt.numel()
+        e1.record(main)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ms_e = float(te.item()) / n_e
+        out["e2e"] = {"ms_per_volume_per_gpu": ms_e, "volumes_per_min": world * 60000.0 / ms_e,
+                      "gvoxel_per_s": world * vol.numel() / ms_e / 1e6, "h2d_bytes_per_volume": host.numel() * 2,
+                      "d2h_bytes_per_volume": ps.product_bytes,
+                      "path": "pinned host volume -> H2D (copy stream, double-buffered) -> PreviewStream.process -> "
+                              "atlases + thumbnails D2H into pinned memory, per rank"}
+    del host, host_out, bufs
+    del vol, ps
+    from paper_2311_15038_b200 import device as dev
+    dev.render_release()
+    torch.cuda.empty_cache()
+    return out
 
 
 def bench_e2e_session(slab, spec, schemes, device, world, dist):
