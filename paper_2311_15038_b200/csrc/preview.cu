@@ -218,8 +218,23 @@ __device__ __forceinline__ void row_atomics(const uint4& q, uint32_t tbl, uint32
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const uint32_t v = __byte_perm(wc, 0u, h ? 0x4432u : 0x4410u);  // one PRMT per voxel
+#ifdef CTP_U16_REL_ADDR
+        // (measured, not the default: 3.903 vs 3.895 ms on config 3 -- one instruction fewer per voxel
+        // buys nothing, the pass is not issue-bound; profiles/r02_u16_rel_addr_ab.txt)
+        // offsets from the table base (hot window first, cold table right behind it): rel =
+        // (v - hot_base) * 128 + 4 * lane wraps far above the window for every bin outside
+        // it, so ONE multiply-add and ONE compare find the hot slot, a predicated
+        // multiply-add (immediate operands) the cold word, and the base rides on the
+        // atomic's uniform operand: PRMT + IMAD + ISETP + @IMAD + ATOMS per voxel (the
+        // absolute-address form below needs one more subtract)
+        constexpr uint32_t kHotBytes = (uint32_t)Vox<uint16_t>::HOT * 128u;
+        const uint32_t rel = v * 128u + lb;  // lb = 4 * lane - hot_base * 128 (mod 2^32)
+        const uint32_t off = rel < kHotBytes ? rel : v * 4u + kHotBytes;
+        o[2 * k + h] = atom_add_shared(tbl + off, kOne);
+#else
         const uint32_t addr = (v - hb < (uint32_t)Vox<uint16_t>::HOT) ? lb + (v << 7) : tbl + (v << 2);
         o[2 * k + h] = atom_add_shared(addr, kOne);
+#endif
       }
     }
   } else {
@@ -444,9 +459,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     tbl = hs_a;
     lb = 4u * (uint32_t)lane;
   } else if constexpr (Vox<uint16_t>::HOT > 0) {
+#ifdef CTP_U16_REL_ADDR
+    tbl = hs_a;                                                          // hot window, then the cold table
+    lb = 4u * (uint32_t)lane - ((uint32_t)hot_base << 7);                // rel = v * 128 + lb
+#else
     // (an opaque copy: keeps the cold-table base in one register, a cold address is one IMAD/LEA)
     asm volatile("mov.u32 %0, %1;" : "=r"(tbl) : "r"(hs_a + 4u * Vox<uint16_t>::HOT * 32));  // cold table
     lb = hs_a + 4u * (uint32_t)lane - ((uint32_t)hot_base << 7);         // hot [slot][lane], slot = v - hot_base
+#endif
   } else {
     tbl = hs_a;
     lb = hs_a + 4u * (uint32_t)(lane % Vox<uint16_t>::COLS);
