@@ -52,6 +52,31 @@ def test_encode_golden(P, golden):
         assert np.array_equal(np.stack(P.encode_slicemaps(back, sset.scheme).atlases), golden[f"enc{i}_out"])
 
 
+def test_encode_decode_seeded_sweep_custom_schemes(P):
+    """40 seeded custom schemes (slicemap.py:52-61 validates grid * s == atlas_dim and map_count ==
+    ceil(s / grid^2); custom schemes are legal, test_slicemap.py:112): grids 1..9 incl. non-powers
+    of two, s with and without 16-byte rows, partial last maps, volumes at s^3 and larger on some
+    axes (downscale first, slicemap.py:130) -- encode equals the oracle byte for byte, decode
+    inverts it, and a volume smaller than s on any axis raises InvalidTarget."""
+    rng = np.random.default_rng(77)
+    for case in range(40):
+        g = int(rng.integers(1, 10))
+        s = int(rng.choice([8, 12, 16, 20, 24, 32, 33, 40, 48, 64]))
+        maps = -(-s // (g * g))
+        scheme = P.SlicemapScheme(s, g * s, g, maps)
+        grow = lambda: int(s if rng.random() < 0.5 else s + rng.integers(1, s + 1))  # noqa: E731
+        shape = (grow(), grow(), grow())
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        sset = P.encode_slicemaps(P.Volume(v), scheme)
+        ref = O.encode_slicemaps(v, (s, g * s, g, maps))
+        assert len(sset.atlases) == maps
+        assert np.array_equal(np.stack(sset.atlases), np.stack(ref)), (case, s, g, shape)
+        assert np.array_equal(P.decode_slicemaps(sset).voxels, O.decode_slicemaps(ref, (s, g * s, g, maps))), (case, s, g)
+    small = P.Volume(np.zeros((16, 16, 12), np.uint8))
+    with pytest.raises(P.InvalidTarget):
+        P.encode_slicemaps(small, P.SlicemapScheme(16, 64, 4, 1))
+
+
 def test_render_golden_bit_exact(P, golden):
     for i in range(int(golden["rv_n"])):
         az, dim, steps, add, thr = golden[f"rv{i}_params"]
@@ -157,6 +182,41 @@ def test_downscale_vector_path_general_ratios(P, cuda):
         v[:, :, :16] = 255  # saturated columns: the packed lanes at their maximum
         got = dev.downscale(torch.from_numpy(v).to(cuda), target).cpu().numpy()
         assert np.array_equal(got, O.downscale(v, target)), (shape, target)
+
+
+def test_downscale_seeded_sweep_every_kernel_path(P, cuda):
+    """80 seeded random (shape, target) pairs through ctp_downscale_u8 against the oracle's
+    volume.py:277-309 restatement, bit for bit: rows that are whole 16-byte vectors (the
+    warp-per-row kernel with x cells <= 2 / 4 / 8 / 16, and the column-sum kernel beyond) and rows
+    that are not (the byte kernel); targets from 1 to n per axis incl. identity axes; random,
+    saturated (the packed 16-bit lanes and the magic-multiplier rounding at their maxima) and
+    sparse data."""
+    from paper_2311_15038_b200 import device as dev
+    rng = np.random.default_rng(2025)
+    for case in range(80):
+        if case % 4 == 3:   # rows that are not whole vectors
+            nx = int(rng.integers(1, 90))
+        else:
+            nx = 16 * int(rng.integers(1, 40))
+        ny, nz = int(rng.integers(1, 48)), int(rng.integers(1, 40))
+        pick = lambda n: int(n if rng.random() < 0.15 else rng.integers(1, n + 1))  # noqa: E731
+        if case % 5 == 0:   # wide x cells (>= 16 columns per output)
+            tx = max(1, nx // int(rng.integers(16, 40)))
+        else:
+            tx = pick(nx)
+        target = (tx, pick(ny), pick(nz))
+        kind = case % 3
+        if kind == 0:
+            v = rng.integers(0, 256, size=(nz, ny, nx), dtype=np.uint8)
+        elif kind == 1:
+            v = np.full((nz, ny, nx), 255, np.uint8)
+            v[rng.random((nz, ny, nx)) < 0.1] = 254
+        else:
+            v = (rng.random((nz, ny, nx)) < 0.07).astype(np.uint8) * rng.integers(1, 256, size=(nz, ny, nx), dtype=np.uint8)
+        if target == (nx, ny, nz):
+            continue  # identity is the host's shortcut (volume.py:290-291)
+        got = dev.downscale(torch.from_numpy(v).to(cuda), target).cpu().numpy()
+        assert np.array_equal(got, O.downscale(v, target)), (case, v.shape, target)
 
 
 def test_errors_match_reference(P):
