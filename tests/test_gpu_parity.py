@@ -87,6 +87,33 @@ def test_render_golden_bit_exact(P, golden):
         assert np.array_equal(img, golden[f"rv{i}_out"]), (i, int(np.abs(img.astype(int) - golden[f"rv{i}_out"]).max()))
 
 
+def test_render_fp64_seeded_sweep_bit_exact(P):
+    """24 seeded views of random anisotropic volumes in the reference's two modes (render.py:125-202):
+    random azimuths incl. the axis-aligned ones, image sizes, step counts, thresholds and gains --
+    bit-identical to the oracle's numba-order restatement (which is pinned to the reference's own
+    renders), through the byte-load path and the texture-gather path alike."""
+    import os
+    rng = np.random.default_rng(404)
+    for case in range(24):
+        shape = tuple(int(x) for x in rng.integers(6, 36, size=3))
+        vol = np.clip(np.rint(rng.normal(70, 60, shape)), 0, 255).astype(np.uint8)
+        if case % 3 == 0:
+            vol[vol < 90] = 0  # sparse: long empty stretches before the first hit
+        az = float(rng.choice([0.0, 90.0, 180.0, 270.0])) if case % 6 == 0 else float(rng.uniform(0, 360))
+        dim, steps = int(rng.integers(16, 40)), int(rng.integers(32, 100))
+        mode = "surface" if case % 2 == 0 else "additive"
+        thr, gain = int(rng.integers(1, 200)), float(rng.choice([1.0, 4.0, 7.5]))
+        p = P.ViewParams(azimuth_deg=az, image_dim=dim, steps=steps, mode=mode, threshold=thr, gain=gain)
+        ref = O.render_view(vol, az, dim, steps, mode, thr, gain)
+        for force in ("0", "1"):  # byte loads / texture gathers
+            os.environ["CTP_RENDER_FP64_TEX"] = force
+            try:
+                img = P.render_view(P.Volume(vol), p)
+            finally:
+                del os.environ["CTP_RENDER_FP64_TEX"]
+            assert np.array_equal(img, ref), (case, shape, az, dim, steps, mode, thr, gain, force)
+
+
 def test_entropy_and_snapshot_golden(P, golden):
     for i in range(int(golden["ent_n"])):
         assert P.image_entropy(golden[f"ent{i}_in"]).entropy == float(golden[f"ent{i}_h"])

@@ -15,6 +15,8 @@ import pytest
 
 from oracle import ctp_oracle as O
 
+ROOT = Path(__file__).resolve().parents[1]
+
 
 # ---------------------------------------------------------------- golden vectors
 
@@ -229,3 +231,75 @@ def test_oracle_viewer_frames_and_bundle_products():
     bins, atl_dp = O.build_data_preview(vol)
     assert sorted(bins) == meta["previews"]["data"]["filtered_bins"]
     assert np.array_equal(np.stack(atl_dp), data)
+
+
+# ------------------------------------------------ the oracle against the LIVE reference (when mounted)
+
+def _live_reference():
+    """ctprev itself, from the mount or from baseline/_ref (neither exists on the GPU box)."""
+    import importlib
+    import os
+    import sys
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/ctp_numba_oracle_live")
+    for d in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (d / "ctprev").is_dir():
+            if str(d) not in sys.path:
+                sys.path.insert(0, str(d))
+            return importlib.import_module("ctprev")
+    pytest.skip("ctprev is neither installed (baseline/_ref) nor mounted")
+
+
+def test_oracle_equals_live_reference_on_the_gpu_sweeps():
+    """The seeded sweeps the GPU tests compare against the oracle (test_gpu_parity.py:
+    test_downscale_seeded_sweep_every_kernel_path, test_encode_decode_seeded_sweep_custom_schemes,
+    test_render_fp64_seeded_sweep_bit_exact) replayed here against ctprev ITSELF: the same
+    generators, the same seeds -- so "GPU == oracle" on the box is "GPU == reference"."""
+    ct = _live_reference()
+    # downscale (volume.py:277-309), a third of the GPU sweep's cases
+    rng = np.random.default_rng(2025)
+    for case in range(80):
+        nx = int(rng.integers(1, 90)) if case % 4 == 3 else 16 * int(rng.integers(1, 40))
+        ny, nz = int(rng.integers(1, 48)), int(rng.integers(1, 40))
+        pick = lambda n: int(n if rng.random() < 0.15 else rng.integers(1, n + 1))  # noqa: E731
+        tx = max(1, nx // int(rng.integers(16, 40))) if case % 5 == 0 else pick(nx)
+        target = (tx, pick(ny), pick(nz))
+        kind = case % 3
+        if kind == 0:
+            v = rng.integers(0, 256, size=(nz, ny, nx), dtype=np.uint8)
+        elif kind == 1:
+            v = np.full((nz, ny, nx), 255, np.uint8)
+            v[rng.random((nz, ny, nx)) < 0.1] = 254
+        else:
+            v = (rng.random((nz, ny, nx)) < 0.07).astype(np.uint8) * rng.integers(1, 256, size=(nz, ny, nx), dtype=np.uint8)
+        if target == (nx, ny, nz) or case % 3:
+            continue
+        assert np.array_equal(O.downscale(v, target), ct.downscale_volume(ct.Volume(v.copy()), target).voxels), case
+    # encode / decode with custom schemes (slicemap.py:120-155)
+    rng = np.random.default_rng(77)
+    for case in range(40):
+        g = int(rng.integers(1, 10))
+        s = int(rng.choice([8, 12, 16, 20, 24, 32, 33, 40, 48, 64]))
+        maps = -(-s // (g * g))
+        grow = lambda: int(s if rng.random() < 0.5 else s + rng.integers(1, s + 1))  # noqa: E731
+        shape = (grow(), grow(), grow())
+        v = rng.integers(0, 256, size=shape, dtype=np.uint8)
+        if case % 4:
+            continue
+        sset = ct.encode_slicemaps(ct.Volume(v.copy()), ct.SlicemapScheme(s, g * s, g, maps))
+        ref = O.encode_slicemaps(v, (s, g * s, g, maps))
+        assert np.array_equal(np.stack(sset.atlases), np.stack(ref)), case
+        assert np.array_equal(ct.decode_slicemaps(sset).voxels, O.decode_slicemaps(ref, (s, g * s, g, maps))), case
+    # fp64 renders (render.py:125-236): every case of the GPU sweep
+    rng = np.random.default_rng(404)
+    for case in range(24):
+        shape = tuple(int(x) for x in rng.integers(6, 36, size=3))
+        vol = np.clip(np.rint(rng.normal(70, 60, shape)), 0, 255).astype(np.uint8)
+        if case % 3 == 0:
+            vol[vol < 90] = 0
+        az = float(rng.choice([0.0, 90.0, 180.0, 270.0])) if case % 6 == 0 else float(rng.uniform(0, 360))
+        dim, steps = int(rng.integers(16, 40)), int(rng.integers(32, 100))
+        mode = "surface" if case % 2 == 0 else "additive"
+        thr, gain = int(rng.integers(1, 200)), float(rng.choice([1.0, 4.0, 7.5]))
+        ref = ct.render_view(ct.Volume(vol.copy()), ct.ViewParams(azimuth_deg=az, image_dim=dim, steps=steps, mode=mode,
+                                                                  threshold=thr, gain=gain))
+        assert np.array_equal(O.render_view(vol, az, dim, steps, mode, thr, gain), ref), (case, shape, az, mode)
