@@ -303,3 +303,53 @@ def test_oracle_equals_live_reference_on_the_gpu_sweeps():
         ref = ct.render_view(ct.Volume(vol.copy()), ct.ViewParams(azimuth_deg=az, image_dim=dim, steps=steps, mode=mode,
                                                                   threshold=thr, gain=gain))
         assert np.array_equal(O.render_view(vol, az, dim, steps, mode, thr, gain), ref), (case, shape, az, mode)
+
+
+def test_oracle_composition_equals_live_reference_on_the_fused_sweep():
+    """The u8 cases of test_gpu_parity.py::test_preview_random_sweep (same generator, same seeds)
+    through ctprev's own functions, composed as SURVEY s8(d) / pipeline.py:215-237, 275 compose
+    them -- volume_histogram, artifact_bins, filter_histogram_bins, _scheme_volume +
+    _pad_to_cube, encode_slicemaps -- against the oracle's ``preview_pipeline``, which is what the
+    fused GPU pass is compared with."""
+    ct = _live_reference()
+    from ctprev.pipeline import _pad_to_cube, _scheme_volume
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_gpu_parity", ROOT / "tests" / "test_gpu_parity.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)  # the GPU sweep's own generator
+    _random_volume = mod._random_volume
+    for case in range(18):
+        rng = np.random.default_rng(1000 + case)
+        dtype = np.uint8 if case % 3 else np.uint16
+        if case < 12:
+            dims = [int(rng.choice([16, 24, 32, 48, 64, 80, 96, 128])) for _ in range(3)]
+            if case % 4 == 3:
+                dims[2] += int(rng.integers(1, 8))
+        else:
+            dims = [int(rng.integers(3, 9)), int(rng.integers(1, 9)), int(rng.choice([1, 5, 8, 16, 17]))]
+        shape = tuple(dims)
+        vox, _ = _random_volume(rng, dtype, shape)
+        if dtype != np.uint8:
+            continue  # the reference rejects uint16 (volume.py:56-57): the extension stays oracle-only
+        big = max(shape)
+        sch = []
+        sizes = [8, 12, 16, 24, 32, 40, 64, 96, 128] if case < 12 else [1, 2, 3, 4, 6, 8]
+        for s in sorted({int(x) for x in rng.choice(sizes, 3)}, reverse=True):
+            if s > big:
+                continue
+            g = int(rng.choice([1, 2, 3, 4, 5, 8]))
+            sch.append((s, g * s, g, -(-s // (g * g))))
+        if not sch:
+            sch = [(1, 2, 2, 1)]
+        hist, bins, f, levels, atl = O.preview_pipeline(vox, [s[0] for s in sch], schemes=sch)
+        v = ct.Volume(vox.copy())
+        assert np.array_equal(ct.volume_histogram(v).bins, hist), case
+        rb = ct.artifact_bins(v)
+        assert rb == bins, case
+        rf = ct.filter_histogram_bins(v, rb)
+        assert np.array_equal(rf.voxels, f), case
+        for (s, a, g, m), lv, at in zip(sch, levels, atl):
+            rl = _scheme_volume(rf, s)
+            assert np.array_equal(rl.voxels, lv), (case, s)
+            sset = ct.encode_slicemaps(_pad_to_cube(rl, s), ct.SlicemapScheme(s, a, g, m))
+            assert np.array_equal(np.stack(sset.atlases), np.stack(at)), (case, s)
