@@ -7,10 +7,12 @@ tools/ref_suite_plugin.py: ``install()`` is called before any test module is imp
 every ``from ctprev.volume import ...`` binds the B200 drop-ins, and the session ends with
 the number of kernels launched through libctprev_b200.so.
 
-The reference's tests are not part of this repository: they are read from the mounted
-reference (this container) or from ``baseline/_ref_tests`` -- a git-ignored copy that
-``tools/r2_ref_suite.sh`` places next to the installed reference (``baseline/_ref``) so that
-it travels to the GPU box; the test is skipped where neither exists."""
+The reference's tests are not part of this repository and are never copied into its history:
+they are read from the mounted reference, or from ``baseline/_ref_tests`` if someone placed
+them next to the installed reference for a GPU run (``tools/r2_ref_suite.sh`` does, into that
+git-ignored directory, and removes nothing else); where neither exists -- the GPU box of a
+plain checkout -- the test is skipped, and the log of the round's run is
+``profiles/r02_ref_suite_under_install.txt`` (141 passed, 49 binding sites, 651 launches)."""
 from __future__ import annotations
 
 import os
