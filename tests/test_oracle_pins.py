@@ -353,3 +353,31 @@ def test_oracle_composition_equals_live_reference_on_the_fused_sweep():
             assert np.array_equal(rl.voxels, lv), (case, s)
             sset = ct.encode_slicemaps(_pad_to_cube(rl, s), ct.SlicemapScheme(s, a, g, m))
             assert np.array_equal(np.stack(sset.atlases), np.stack(at)), (case, s)
+
+
+def test_slice_cells_equal_the_viewer_parity_fixture():
+    """frontend/tests/fixtures/parity.json (every slice -> (map, cx, cy) for the planned schemes
+    128 / 256 / 512): the mirror's ``slice_cell`` (slicemap.py:79-85) and the
+    oracle's atlas layout agree with every entry.  Read from the mounted reference (skipped where
+    it is absent; the fixture is not copied)."""
+    import json
+    import paper_2311_15038_b200 as P
+    fx = Path("/root/reference/pkg/frontend/tests/fixtures/parity.json")
+    if not fx.is_file():
+        pytest.skip("the reference's frontend fixtures are not mounted")
+    table = json.loads(fx.read_text())
+    for key, cells in table.items():
+        s = int(key)
+        scheme = P.plan_scheme(s)
+        assert len(cells) == s
+        for k, (m, cx, cy) in enumerate(cells):
+            assert P.slice_cell(k, scheme) == (m, cx, cy), (s, k)
+        sc = O.plan_scheme(s)
+        g = sc[2]
+        for k in (0, 1, g - 1, g, g * g - 1, g * g, s - 1):
+            m, cx, cy = cells[k]
+            vol = np.zeros((s, s, s), np.uint8)
+            vol[k, 3, 5] = 200
+            atl = O.encode_slicemaps(vol, sc)
+            # a single voxel of slice k lands in that cell of that map, and nowhere else
+            assert atl[m][cy * s + 3, cx * s + 5] == 200 and int(np.stack(atl).astype(np.int64).sum()) == 200, (s, k)
