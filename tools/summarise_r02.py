@@ -106,7 +106,7 @@ def launches(tag: str) -> None:
         cnt[key] += 1
     allt = sum(tot.values())
     lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 20 --warmup 3 "
-             "--no-mip --no-cpu-baseline --no-configs --no-e2e",
+             "--no-mip --no-cpu-baseline --no-configs --no-e2e --no-sustained",
              "# (cold-cache, serialised per-launch times; the SHARE of the step is what compares with the bench).",
              "# The timed c2 step is ONE preview_kernel launch on grid (148,1,1) (artifact-LUT phase + fused pass);",
              "# synth_kernel generates the volume once.",
